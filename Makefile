@@ -1,0 +1,32 @@
+# Builds the B200-native HashGraph engine in-tree (the .so travels to the GPU box).
+#   paper_1907_02900_b200/libhg_b200.so   CUDA kernels + C-ABI (include/hg_b200.h)
+#   oracle/_build, oracle/_ref            test-only parity checkers (oracle/Makefile)
+NVCC ?= /usr/local/cuda/bin/nvcc
+PKG := paper_1907_02900_b200
+SRC := $(wildcard $(PKG)/csrc/*.cu)
+HDR := $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.h) include/hg_b200.h
+OBJ := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
+           --expt-relaxed-constexpr -Iinclude $(EXTRA_NVFLAGS)
+
+all: $(PKG)/libhg_b200.so oracle
+
+build/%.o: $(PKG)/csrc/%.cu $(HDR)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(PKG)/libhg_b200.so: $(OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart_static -Xlinker --no-undefined -lrt -ldl -lpthread
+
+oracle:
+	$(MAKE) -s -f oracle/Makefile
+
+ptxas:
+	@for f in $(SRC); do $(NVCC) $(NVFLAGS) -Xptxas -v -c $$f -o /dev/null 2>&1 | grep -E "Function properties|registers|spill" ; done
+
+clean:
+	rm -rf build $(PKG)/libhg_b200.so
+	$(MAKE) -s -f oracle/Makefile clean
+
+.PHONY: all oracle clean ptxas

@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""HashGraph build + probe benchmark (BASELINE.json metric, config C2).
+
+One step = one pass of the hot path over one batch of synthetic input:
+  build a HashGraph over N = 2^28 uniform u32 keys (splitmix64 seed 1, load 1,
+  binned V2 build unless --variant 1), then probe_standard with M = 2^28
+  independent u32 probe keys (splitmix64 seed 2), count only (ProbeOptions{}).
+value = (N + M) / step time in G keys/s, inputs resident in HBM; e2e = the
+same step through the public API with the keys and probes in pinned HOST
+memory (H2D inside the timed region, result scalars read back).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Under torchrun (N > 1) the table is sharded by hash range (weak scaling: each
+rank contributes N keys and M probes); see paper_1907_02900_b200/sharded.py.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "build and probe Gkeys/s (2^28 uint32 keys) at 1/2/4/8 B200; % of HBM roofline"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--log2n", type=int, default=28)
+    p.add_argument("--variant", type=int, default=2, choices=[1, 2])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-extras", action="store_true", help="skip the per-phase/variant breakdown")
+    p.add_argument("--cpu-log2n", type=int, default=22)
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+
+def splitmix_u32(seed: int, start: int, n: int) -> np.ndarray:
+    """SURVEY.md Appendix B generator on the host (numpy, wrapping u64)."""
+    with np.errstate(over="ignore"):
+        i = np.arange(start + 1, start + n + 1, dtype=np.uint64)
+        z = np.uint64(seed) + i * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return (z & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock/throttle sampling (NVML) during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def alg_bytes(name: str, n: int, v: int, m: int, c: int, kb: int = 4, vb: int = 4,
+              ob: int = 4) -> int:
+    """Algorithmic bytes of one launch at array granularity (SURVEY.md 8(d)
+    convention: each pass reads each input array once and writes each output
+    once; an atomically updated array counts read + write). DESIGN.md lists
+    the same table."""
+    return {
+        "k1_hash_count": n * kb + 2 * v * ob,
+        "k2_scan": 2 * v * ob,
+        "k3_scatter": n * kb + 2 * v * ob + n * (kb + vb),
+        "k4_part_hist": n * kb,
+        "k5_part_scan": 0,
+        "k6_part_scatter": n * kb + n * (kb + vb),
+        "k7_part_build": 2 * n * (kb + vb) + v * ob,
+        "k8_probe_count": m * kb + (v + 1) * ob + c * kb,
+    }.get(name, 0)
+
+
+# ------------------------------------------------------------------ reference arm
+
+def cpu_reference_rate(variant: int, log2n: int, trials: int, warmup: int):
+    """The reference's own CPU implementation (oracle/_ref = the unmodified
+    reference headers; oracle port when _ref is absent) on the host cores:
+    build + probe_standard of a 2^log2n sample of the same workload."""
+    from oracle.oracle import Oracle, Reference, have_reference
+    n = 1 << log2n
+    keys = splitmix_u32(1, 0, n).astype(np.uint64)
+    probes = splitmix_u32(2, 0, n).astype(np.uint64)
+    threads = os.cpu_count() or 1
+    if have_reference():
+        ref, kind = Reference(), "reference"
+        ref.set_threads(threads)
+
+        def one():
+            h = ref.build_handle(keys, variant=variant)
+            r = ref.probe(h, probes)
+            ref.free(h)
+            return r["match_count"]
+    else:  # pragma: no cover - the GPU box ships the prebuilt oracle/_ref
+        ref, kind, threads = Oracle(), "port", 1
+
+        def one():
+            t = ref.build(keys, variant=variant)
+            return ref.probe_standard(t, probes)["match_count"]
+    for _ in range(warmup):
+        one()
+    times = []
+    for _ in range(trials):
+        t0 = time.perf_counter()
+        one()
+        times.append(time.perf_counter() - t0)
+    med = statistics.median(times)
+    return {"value": 2 * n / med / 1e9, "unit": "Gkeys/s", "cores": threads, "kind": kind,
+            "sample": f"build_v{variant} + probe_standard (count) of 2^{log2n} u32 keys "
+                      f"(splitmix seed 1) and 2^{log2n} probes (seed 2), load 1; median of "
+                      f"{trials} after {warmup} warm-up; HASHGRAPH_THREADS={threads}",
+            "seconds_median": med, "seconds": times}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps = max(1, args.steps)
+    res = cpu_reference_rate(args.variant, args.cpu_log2n, steps, args.warmup)
+    n = 1 << args.cpu_log2n
+    line = {
+        "impl": "reference", "metric": METRIC, "value": res["value"], "unit": "Gkeys/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": res["seconds_median"] * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"C2 sample on host cores: build_v{args.variant} + "
+                               f"probe_standard, 2^{args.cpu_log2n} u32 keys + probes, load 1",
+                   "n": n, "m": n, "load_factor": 1.0, "variant": args.variant},
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": res["value"], "unit": "Gkeys/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ B200 arm
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1907_02900_b200 as hg
+    from paper_1907_02900_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = m = 1 << args.log2n
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    keys = torch.empty(n, dtype=torch.int32, device=dev)
+    probes = torch.empty(m, dtype=torch.int32, device=dev)
+    hg.generate(keys, kind=0, seed=1, start=rank * n)
+    hg.generate(probes, kind=0, seed=2, start=rank * m)
+    result = torch.zeros(2, dtype=torch.int64, device=dev)
+    build = hg.build_v2 if args.variant == 2 else hg.build_v1
+
+    if world > 1:
+        from paper_1907_02900_b200 import sharded
+        engine = sharded.ShardedHashGraph(world, rank, variant=args.variant)
+
+        def step():
+            engine.build_and_probe(keys, probes, result)
+    else:
+        def step():
+            t = build(keys, stream=sp)
+            hg.probe_device(t, probes, result, stream=sp)
+            t.close(sp)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    nv = hg.derived_vertex_count(n, 1.0)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region (device-resident inputs; each input 1 GiB > 126 MB L2)
+    _lib.profiler_enable(True)
+    _lib.profiler_collect()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    barrier()
+    with clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+    _lib.profiler_enable(False)
+    kern = _lib.profiler_collect()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * (n + m) / (ms * 1e-3) / 1e9
+    matches, comparisons = (int(x) for x in result.cpu().tolist())
+    gpu_launches = sum(l for (l, _) in kern.values())
+
+    # ---- roofline of the dominant kernel (algorithmic bytes / avg launch time)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks else "fallback 6.65 TB/s"
+    local_n = n if world == 1 else int(engine.last_local_n)
+    local_m = m if world == 1 else int(engine.last_local_m)
+    local_v = nv if world == 1 else int(engine.local_vertices)
+    dom = max((k for k in kern if alg_bytes(k, 1, 1, 1, 1) > 0), key=lambda k: kern[k][1])
+    dl, dms = kern[dom]
+    avg_ms = dms / dl
+    ab = alg_bytes(dom, local_n, local_v, local_m, comparisons if world == 1 else
+                   int(engine.last_local_c))
+    achieved = ab / (avg_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "alg_bytes_per_launch": ab, "avg_launch_ms": round(avg_ms, 4),
+                "peak_source": peak_src,
+                "step_alg_bytes": sum(alg_bytes(k, local_n, local_v, local_m, comparisons) * kern[k][0]
+                                      for k in kern) // max(1, args.steps)}
+    kernels = {k: {"launches": l, "avg_ms": round(t / l, 4), "share": round(t / sum(
+        x[1] for x in kern.values()), 4)} for k, (l, t) in sorted(kern.items(), key=lambda x: -x[1][1])}
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "Gkeys/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic",
+        "config": {"workload": f"C2: build_v{args.variant} over 2^{args.log2n} uniform u32 keys "
+                               f"(splitmix64 seed 1) at load 1 + probe_standard (count) of "
+                               f"2^{args.log2n} u32 probes (seed 2), per GPU",
+                   "n_per_gpu": n, "m_per_gpu": m, "load_factor": 1.0, "variant": args.variant,
+                   "vertices": nv * (1 if world == 1 else 1),
+                   "l2": "inputs larger than L2 (1 GiB keys + 1 GiB probes per GPU vs 126 MB L2)",
+                   "parallelism": f"hash-range shards x{world}" if world > 1 else "1 GPU"},
+        "roofline": roofline,
+        "clocks": clocks.summary(),
+        "gpu_launches": gpu_launches,
+        "match_count": matches, "key_comparisons": comparisons,
+        "kernels": kernels,
+    }
+
+    # ---- per-phase / per-variant breakdown (device-resident, outside the timed region)
+    if not args.no_extras and world == 1:
+        extras = {}
+        for var, bfn in ((1, hg.build_v1), (2, hg.build_v2)):
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            reps = 3
+            tb = tp = 0.0
+            for _ in range(reps):
+                e0.record(stream)
+                t = bfn(keys, stream=sp)
+                e1.record(stream)
+                hg.probe_device(t, probes, result, stream=sp)
+                e2.record(stream)
+                t.close(sp)
+                torch.cuda.synchronize()
+                tb += e0.elapsed_time(e1)
+                tp += e1.elapsed_time(e2)
+            extras[f"v{var}"] = {"build_ms": round(tb / reps, 4),
+                                 "build_gkeys_s": round(n / (tb / reps * 1e-3) / 1e9, 3),
+                                 "probe_ms": round(tp / reps, 4),
+                                 "probe_gkeys_s": round(m / (tp / reps * 1e-3) / 1e9, 3)}
+        line["phases"] = extras
+
+    # ---- e2e through the public API with pinned HOST buffers
+    if not args.no_e2e and world == 1:
+        hkeys = keys.cpu().pin_memory()
+        hprobes = probes.cpu().pin_memory()
+        torch.cuda.synchronize()
+
+        def e2e_step():
+            t = build(hkeys, stream=sp)           # H2D of the keys inside hg_build
+            r = hg.probe_standard(t, hprobes)     # H2D of probes, D2H of the totals, sync
+            t.close(sp)
+            return r
+
+        e2e_step()
+        e2e_step()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            r = e2e_step()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = f0.elapsed_time(f1) / args.steps
+        assert r.match_count == matches, "e2e result differs from device-resident result"
+        line["e2e"] = {"value": round((n + m) / (e_ms * 1e-3) / 1e9, 3), "unit": "Gkeys/s",
+                       "ms_per_step": round(e_ms, 3), "h2d_bytes_per_step": 4 * (n + m),
+                       "d2h_bytes_per_step": 16,
+                       "path": "hashgraph.build_v2/probe_standard -> C-ABI hg_build/hg_probe "
+                               "with pinned host buffers"}
+
+    if not args.no_cpu and world == 1 and rank == 0:
+        try:
+            cb = cpu_reference_rate(args.variant, args.cpu_log2n, trials=5, warmup=1)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as ex:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "error": str(ex)}
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

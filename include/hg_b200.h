@@ -1,0 +1,184 @@
+/*
+ * hg_b200.h -- C-ABI of the B200-native HashGraph engine (libhg_b200.so).
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj/include/hashgraph, header-only C++20). The reference
+ * has no FFI of its own; each entry point below names the reference
+ * interface it replaces (file:line), and include/hashgraph/ headers re-export
+ * the reference's C++ names on top of these calls.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no exceptions cross this boundary.
+ *  - Every array argument may live in host memory (pageable or pinned) or in
+ *    device memory of the current CUDA device; the library detects which and
+ *    stages host data through the device in stream order.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *  - Calls are stream-ordered. A call that returns host-visible scalars
+ *    (hg_probe without device_result, hg_count_instances, hg_validate,
+ *    hg_table_export into host memory) synchronises `stream` first.
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    call fails with HG_ECUDA.
+ */
+#ifndef HG_B200_H
+#define HG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HG_ABI_VERSION 1
+
+/* Error model. Replaces the reference's exceptions:
+ *   std::invalid_argument (core.hpp:106-109 check_config, join.hpp:145-147) -> HG_EINVAL
+ *   std::out_of_range     (core.hpp:88-90 vertex_entries)                   -> HG_ERANGE
+ *   std::overflow_error   (parallel.hpp:153,171,178)                        -> HG_EOVERFLOW */
+typedef enum hg_status {
+    HG_OK = 0,
+    HG_EINVAL = 1,
+    HG_ERANGE = 2,
+    HG_EOVERFLOW = 3,
+    HG_ENOMEM = 4,
+    HG_ECUDA = 5,
+    HG_ENCCL = 6,
+    HG_EUNSUPPORTED = 7
+} hg_status;
+
+typedef enum hg_hash_kind {
+    HG_HASH_MIX64 = 0,    /* VertexHasher: mix64(key ^ seed) % V (hash.hpp:27-34) */
+    HG_HASH_IDENTITY = 1  /* key % V; the fixture hasher of tests/support.hpp:42-46 */
+} hg_hash_kind;
+
+typedef enum hg_variant {
+    HG_BUILD_SIMPLE = 1, /* build_v1 (core.hpp:160-177) */
+    HG_BUILD_BINNED = 2  /* build_v2 (core.hpp:183-230) */
+} hg_variant;
+
+/* BuildConfig (core.hpp:30-35) + the optional vertex_count override of
+ * build_v1/build_v2 (core.hpp:165-166) + device knobs. */
+typedef struct hg_build_config {
+    double load_factor;          /* V = max(1, floor(N / load_factor)) (core.hpp:59-63) */
+    uint64_t bin_count;          /* validated (>= 1, core.hpp:108); CPU-cache tuning knob */
+    uint64_t hash_seed;          /* core.hpp:33 */
+    uint64_t vertex_count;       /* 0 = derive from load_factor */
+    int32_t variant;             /* hg_variant */
+    int32_t hash_kind;           /* hg_hash_kind */
+    int32_t stable;              /* 1 = ExecMode::sequential layout: segments in input order */
+    int32_t aggregate;           /* warp-aggregated atomics: -1 auto, 0 off, 1 on */
+    uint64_t partition_vertices; /* binned build partition width (power of two); 0 = auto */
+} hg_build_config;
+
+/* Defaults of BuildConfig{} (core.hpp:30-35): load 1.0, bins 2^15, seed 0,
+ * parallel mode (stable = 0), variant HG_BUILD_SIMPLE. */
+void hg_build_config_init(hg_build_config* cfg);
+
+/* derived_vertex_count (core.hpp:59-63). HG_EINVAL when load_factor <= 0. */
+hg_status hg_derived_vertex_count(uint64_t n, double load_factor, uint64_t* out);
+
+/* hash_to_vertex (hash.hpp:36-39) for a single key, host-side convenience
+ * (the table paths evaluate the same function on the device). */
+uint64_t hg_hash_to_vertex(uint64_t key, uint64_t seed, uint64_t num_vertices);
+
+typedef struct hg_table hg_table;
+
+/* build_v1 / build_v2 (core.hpp:173-177, :226-230 and the hasher-templated
+ * overloads :160-171, :183-224).
+ *   keys       n keys of key_width bytes (4 = u32, 8 = u64; u32 keys are
+ *              zero-extended before hashing, exactly as the reference's
+ *              u64-only API would see them)
+ *   vals       NULL: each entry's value is its input position (Entry::index,
+ *              core.hpp:21-26); else n values of val_width (4|8) bytes
+ * On success *out owns the device-resident CSR table. */
+hg_status hg_build(const void* keys, int32_t key_width, const void* vals, int32_t val_width,
+                   uint64_t n, const hg_build_config* cfg, void* stream, hg_table** out);
+
+typedef struct hg_table_info {
+    uint64_t num_vertices; /* HashGraph::num_vertices (core.hpp:79) */
+    uint64_t num_edges;    /* HashGraph::num_edges (core.hpp:80) */
+    uint64_t hash_seed;    /* core.hpp:83 */
+    double load_factor;    /* core.hpp:84 */
+    int32_t key_width;
+    int32_t val_width;
+    int32_t off_width;     /* device offsets width (4 when N < 2^32 and V <= 2^32) */
+    int32_t hash_kind;
+} hg_table_info;
+
+hg_status hg_table_get_info(const hg_table* t, hg_table_info* info);
+
+/* Zero-copy device views of the SoA CSR (offsets[V+1], keys[N], vals[N]). */
+hg_status hg_table_device_arrays(const hg_table* t, const void** offsets, const void** keys,
+                                 const void** vals);
+
+/* HashGraph::offsets()/edges() (core.hpp:81-82) in the reference layout,
+ * widened to u64: offsets[V+1], keys[N], vals[N] (any may be NULL). */
+hg_status hg_table_export(const hg_table* t, uint64_t* offsets, uint64_t* keys, uint64_t* vals,
+                          void* stream);
+
+/* Frees the table's device buffers in stream order. */
+hg_status hg_table_destroy(hg_table* t, void* stream);
+
+/* ProbeOptions (join.hpp:25-28) + device output knobs. */
+typedef struct hg_probe_options {
+    int32_t materialize;     /* collect pairs (join.hpp:26) */
+    int32_t pair_width;      /* 8: MatchPair{u64 left, u64 right} layout (join.hpp:18-23); 4: u32 pairs */
+    uint64_t pair_cap;       /* join.hpp:27, default 2^24 */
+    void* pairs;             /* >= pair_cap pairs; host or device */
+    uint32_t* counts;        /* nullable: per-probe match counts (count_instances per key) */
+    uint64_t* device_result; /* nullable device u64[2] {match_count, key_comparisons}; when set
+                                the call is fully asynchronous (result is zeroed) */
+} hg_probe_options;
+
+void hg_probe_options_init(hg_probe_options* opts);
+
+/* JoinResult (join.hpp:30-35). */
+typedef struct hg_probe_result {
+    uint64_t match_count;     /* exact, independent of materialisation */
+    uint64_t key_comparisons; /* full-key comparisons = sum of probed segment lengths */
+    uint64_t pairs_written;   /* min(match_count, pair_cap) when materialising */
+    int32_t truncated;        /* match_count > pair_cap */
+} hg_probe_result;
+
+/* probe_standard (join.hpp:110-136). Pairs are (left = build entry value,
+ * right = probe position) (join.hpp:125), written to deterministic slots in
+ * probe order; under a cap the first pair_cap slots are kept. probe_width
+ * must equal the table's key width or be 4 for a u64-keyed table. */
+hg_status hg_probe(const hg_table* t, const void* probes, int32_t probe_width, uint64_t m,
+                   const hg_probe_options* opts, hg_probe_result* result, void* stream);
+
+/* count_instances (core.hpp:235-246). */
+hg_status hg_count_instances(const hg_table* t, uint64_t key, uint64_t* out, void* stream);
+
+/* validate_csr (core.hpp:251-287) on the device, plus (input_keys != NULL)
+ * the check keys[j] == input_keys[vals[j]]. *violation = 0 when valid, else
+ * the code of the first violated invariant (see hg_util.cu). */
+hg_status hg_validate(const hg_table* t, const void* input_keys, uint64_t expected_entries,
+                      int32_t* violation, void* stream);
+
+/* Synthetic inputs: kind 0 = (u32|u64)splitmix64(seed, start+i);
+ * kind 1 = C4 probes with hit ratio `hit` over ref[n_ref]; kind 2 = scramble31(start+i). */
+hg_status hg_generate(void* out, int32_t key_width, uint64_t n, int32_t kind, uint64_t seed,
+                      uint64_t start, double hit, const void* ref, uint64_t n_ref, void* stream);
+
+/* Kernel timeline (tracing): when enabled, every engine kernel launch is
+ * bracketed by CUDA events on its stream. collect() waits for the recorded
+ * events, aggregates per kernel name, clears the log and returns the number
+ * of distinct kernels (entries beyond max_out are dropped). */
+typedef struct hg_kernel_time {
+    char name[48];
+    uint64_t launches;
+    double total_ms;
+} hg_kernel_time;
+
+void hg_profiler_enable(int32_t on);
+int32_t hg_profiler_collect(hg_kernel_time* out, int32_t max_out);
+
+/* Last error message of the calling thread. */
+const char* hg_last_error(void);
+int32_t hg_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HG_B200_H */

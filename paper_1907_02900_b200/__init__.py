@@ -1,0 +1,19 @@
+"""B200-native HashGraph engine (Green, arXiv 1907.02900).
+
+Drop-in for the reference's hot path (proj/include/hashgraph: build_v1,
+build_v2, probe_standard): hand-written sm_100a CUDA kernels behind the C-ABI
+in include/hg_b200.h, with this package as the Python mirror of the reference
+API and the C++ mirror in include/hashgraph/.
+"""
+from .hashgraph import (ENTRY_DTYPE, MATCH_PAIR_DTYPE, BuildConfig, BuildStats, ExecMode,
+                        HashGraph, IdentityHasher, InvalidArgument, JoinResult, OutOfRange,
+                        Overflow, ProbeOptions, VertexHasher, build_v1, build_v2, count_instances,
+                        derived_vertex_count, generate, hash_to_vertex, probe_standard,
+                        validate_csr)
+
+__all__ = [
+    "ENTRY_DTYPE", "MATCH_PAIR_DTYPE", "BuildConfig", "BuildStats", "ExecMode", "HashGraph",
+    "IdentityHasher", "InvalidArgument", "JoinResult", "OutOfRange", "Overflow", "ProbeOptions",
+    "VertexHasher", "build_v1", "build_v2", "count_instances", "derived_vertex_count", "generate",
+    "hash_to_vertex", "probe_standard", "validate_csr",
+]

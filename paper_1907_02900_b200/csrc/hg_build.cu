@@ -1,0 +1,316 @@
+// hg_build.cu -- HashGraph table construction on sm_100a.
+//
+// Simple build (V1), replacing proj/include/hashgraph/core.hpp:120-177
+// (detail::create_table + build_v1):
+//   K1 k_hash_count  counts[h(k)]++            (core.hpp:126-133)
+//   K2 scan          exclusive scan, in place  (core.hpp:135 -> parallel.hpp:141-192)
+//   K3 k_scatter     pos = cursor[h(k)]++      (core.hpp:137-150)
+// One (V+1)-entry array serves as counter, offsets and placement cursor:
+// K1 counts vertex v into offs[v+1]; the in-place exclusive scan turns
+// offs[v+1] into start(v); K3's fetch-add on offs[v+1] hands out slots
+// start(v)..end(v)-1 and leaves offs[v+1] == end(v) == start(v+1), i.e. the
+// finished CSR offsets (offs[0] stays 0). This drops the reference's separate
+// counter zeroing (core.hpp:137) and offsets gather from the placement pass.
+//
+// Binned build (V2, core.hpp:183-230) lives in hg_binned.cu. The optional
+// "stable" post-pass (k_seg_sort_*) orders every segment by input index,
+// which is exactly the reference's ExecMode::sequential layout
+// (core.hpp:115-119: sequential placement keeps source order).
+#include <algorithm>
+#include <cstdio>
+
+#include "hg_common.cuh"
+#include "hg_internal.h"
+#include "hg_scan.cuh"
+
+namespace hg {
+
+int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+template <typename Kern>
+static unsigned persistent_grid(Kern k, int block, size_t smem, uint64_t work_items) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, block, smem);
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t cap = uint64_t(per_sm) * num_sms();
+    const uint64_t need = (work_items + block - 1) / block;
+    return unsigned(std::max<uint64_t>(1, std::min(cap, need)));
+}
+
+// Grid-stride loop over keys with 16-byte vector loads (two in flight per
+// thread), calling f(i, key) for every key. Lanes of a warp stay converged
+// inside f except in the unaligned head / ragged tail.
+template <typename K, typename F>
+__device__ __forceinline__ void for_each_key(const K* __restrict__ keys, uint64_t n, F&& f) {
+    constexpr int VEC = 16 / sizeof(K);
+    using V = typename std::conditional<sizeof(K) == 4, uint4, ulonglong2>::type;
+    const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    uint64_t head = ((16 - (reinterpret_cast<uintptr_t>(keys) & 15)) & 15) / sizeof(K);
+    if (head > n) head = n;
+    if (gtid < head) f(gtid, keys[gtid]);
+    const uint64_t nvec = (n - head) / VEC;
+    const V* body = reinterpret_cast<const V*>(keys + head);
+    uint64_t q = gtid;
+    for (; q + stride < nvec; q += 2 * stride) {
+        const V a = __ldcs(body + q);
+        const V b = __ldcs(body + q + stride);
+        const K* ka = reinterpret_cast<const K*>(&a);
+        const K* kb = reinterpret_cast<const K*>(&b);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) f(head + q * VEC + k, ka[k]);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) f(head + (q + stride) * VEC + k, kb[k]);
+    }
+    if (q < nvec) {
+        const V a = __ldcs(body + q);
+        const K* ka = reinterpret_cast<const K*>(&a);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) f(head + q * VEC + k, ka[k]);
+    }
+    const uint64_t done = head + nvec * VEC;
+    if (gtid < n - done) f(done + gtid, keys[done + gtid]);
+}
+
+// ---------------------------------------------------------------- K1 / K3
+
+template <typename K, typename OffT, bool POW2>
+__global__ void __launch_bounds__(256)
+k_hash_count(const K* __restrict__ keys, uint64_t n, uint64_t seed, int hk, Divisor nv,
+             OffT* __restrict__ cnt, int aggregate) {
+    constexpr bool V32 = sizeof(OffT) == 4;
+    for_each_key(keys, n, [&](uint64_t, K key) {
+        const uint64_t v = hk == kHashIdentity ? vertex_of<kHashIdentity, POW2>(key, seed, nv)
+                                               : vertex_of<kHashMix64, POW2>(key, seed, nv);
+        if (aggregate) {
+            aggregated_count<V32>(cnt + v, __activemask(), v);
+        } else {
+            red_add(cnt + v, OffT(1));
+        }
+    });
+}
+
+template <typename K, typename VT, typename OffT, bool POW2>
+__global__ void __launch_bounds__(256)
+k_scatter(const K* __restrict__ keys, const VT* __restrict__ vals, uint64_t n, uint64_t seed,
+          int hk, Divisor nv, OffT* __restrict__ cursor, K* __restrict__ okeys,
+          VT* __restrict__ ovals, int aggregate) {
+    constexpr bool V32 = sizeof(OffT) == 4;
+    for_each_key(keys, n, [&](uint64_t i, K key) {
+        const uint64_t v = hk == kHashIdentity ? vertex_of<kHashIdentity, POW2>(key, seed, nv)
+                                               : vertex_of<kHashMix64, POW2>(key, seed, nv);
+        OffT pos;
+        if (aggregate) {
+            pos = aggregated_ticket<V32>(cursor + v, __activemask(), v);
+        } else {
+            pos = atom_add(cursor + v, OffT(1));
+        }
+        okeys[pos] = key;
+        ovals[pos] = vals ? vals[i] : VT(i);
+    });
+}
+
+// --------------------------------------------------- stable segment order
+// Sequential-mode layout (core.hpp:115-119): every segment in ascending input
+// index. Short segments: one thread, insertion sort. Long segments: one CTA,
+// an ascending-only bitonic network (valid for any length: the implicit +inf
+// padding never moves, so comparators touching it are skipped).
+
+constexpr int kSmallSeg = 16;
+constexpr int kSmemSeg = 2048;
+
+template <typename K, typename VT, typename OffT>
+__global__ void __launch_bounds__(256)
+k_seg_sort_small(const OffT* __restrict__ offs, uint64_t nv, K* keys, VT* vals,
+                 uint64_t* big_list, unsigned long long* big_n) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < nv; v += stride) {
+        const uint64_t b = offs[v], e = offs[v + 1];
+        const uint64_t len = e - b;
+        if (len <= 1) continue;
+        if (len > kSmallSeg) {
+            big_list[atomicAdd(big_n, 1ull)] = v;
+            continue;
+        }
+        K kk[kSmallSeg];
+        VT vv[kSmallSeg];
+        for (uint32_t t = 0; t < len; ++t) {
+            kk[t] = keys[b + t];
+            vv[t] = vals[b + t];
+        }
+        for (uint32_t t = 1; t < len; ++t) {
+            const K ck = kk[t];
+            const VT cv = vv[t];
+            int u = int(t) - 1;
+            while (u >= 0 && vv[u] > cv) {
+                kk[u + 1] = kk[u];
+                vv[u + 1] = vv[u];
+                --u;
+            }
+            kk[u + 1] = ck;
+            vv[u + 1] = cv;
+        }
+        for (uint32_t t = 0; t < len; ++t) {
+            keys[b + t] = kk[t];
+            vals[b + t] = vv[t];
+        }
+    }
+}
+
+template <typename K, typename VT>
+__device__ __forceinline__ void cmp_swap(K* k, VT* v, uint64_t i, uint64_t j) {
+    if (v[j] < v[i]) {
+        const VT tv = v[i];
+        v[i] = v[j];
+        v[j] = tv;
+        const K tk = k[i];
+        k[i] = k[j];
+        k[j] = tk;
+    }
+}
+
+template <typename K, typename VT>
+__device__ void block_bitonic_by_val(K* k, VT* v, uint64_t len) {
+    uint64_t p2 = 1;
+    while (p2 < len) p2 <<= 1;
+    const uint64_t pairs = p2 / 2;
+    for (uint64_t size = 2; size <= p2; size <<= 1) {
+        const uint64_t h = size / 2;
+        for (uint64_t t = threadIdx.x; t < pairs; t += blockDim.x) {
+            const uint64_t blk = t / h, off = t % h;
+            const uint64_t i = blk * size + off, j = blk * size + size - 1 - off;
+            if (j < len) cmp_swap(k, v, i, j);
+        }
+        __syncthreads();
+        for (uint64_t half = h / 2; half >= 1; half >>= 1) {
+            for (uint64_t t = threadIdx.x; t < pairs; t += blockDim.x) {
+                const uint64_t blk = t / half, off = t % half;
+                const uint64_t i = blk * 2 * half + off, j = i + half;
+                if (j < len) cmp_swap(k, v, i, j);
+            }
+            __syncthreads();
+        }
+    }
+}
+
+template <typename K, typename VT, typename OffT>
+__global__ void __launch_bounds__(512)
+k_seg_sort_big(const OffT* __restrict__ offs, K* keys, VT* vals, const uint64_t* list,
+               const unsigned long long* list_n) {
+    __shared__ K sk[kSmemSeg];
+    __shared__ VT sv[kSmemSeg];
+    const uint64_t cnt = *list_n;
+    for (uint64_t it = blockIdx.x; it < cnt; it += gridDim.x) {
+        const uint64_t v = list[it];
+        const uint64_t b = offs[v], len = uint64_t(offs[v + 1]) - b;
+        if (len <= kSmemSeg) {
+            for (uint64_t t = threadIdx.x; t < len; t += blockDim.x) {
+                sk[t] = keys[b + t];
+                sv[t] = vals[b + t];
+            }
+            __syncthreads();
+            block_bitonic_by_val(sk, sv, len);
+            for (uint64_t t = threadIdx.x; t < len; t += blockDim.x) {
+                keys[b + t] = sk[t];
+                vals[b + t] = sv[t];
+            }
+            __syncthreads();
+        } else {
+            block_bitonic_by_val(keys + b, vals + b, len);
+            __threadfence_block();
+            __syncthreads();
+        }
+    }
+}
+
+template <typename K, typename VT, typename OffT>
+static cudaError_t stable_order(const TableDesc& t, cudaStream_t s) {
+    if (t.n < 2) return cudaSuccess;
+    const uint64_t cap = t.n / (kSmallSeg + 1) + 1;
+    void* scratch = nullptr;
+    cudaError_t e = cudaMallocAsync(&scratch, (cap + 1) * sizeof(uint64_t), s);
+    if (e != cudaSuccess) return e;
+    uint64_t* list = static_cast<uint64_t*>(scratch);
+    auto* list_n = reinterpret_cast<unsigned long long*>(list + cap);
+    cudaMemsetAsync(list_n, 0, 8, s);
+    const unsigned g1 = persistent_grid(k_seg_sort_small<K, VT, OffT>, 256, 0, t.nv);
+    HG_LAUNCH("seg_sort_small", s, k_seg_sort_small<K, VT, OffT><<<g1, 256, 0, s>>>(static_cast<const OffT*>(t.offs), t.nv,
+                                                    static_cast<K*>(t.keys),
+                                                    static_cast<VT*>(t.vals), list, list_n));
+    HG_LAUNCH("seg_sort_big", s, k_seg_sort_big<K, VT, OffT><<<num_sms() * 2, 512, 0, s>>>(
+        static_cast<const OffT*>(t.offs), static_cast<K*>(t.keys), static_cast<VT*>(t.vals), list,
+        list_n));
+    e = cudaGetLastError();
+    cudaFreeAsync(scratch, s);
+    return e;
+}
+
+// ------------------------------------------------------------------ V1
+
+template <typename K, typename VT, typename OffT, bool POW2>
+static cudaError_t build_v1_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s) {
+    const Divisor nv = make_divisor(t.nv);
+    OffT* offs = static_cast<OffT*>(t.offs);
+    cudaError_t e = cudaMemsetAsync(offs, 0, (t.nv + 1) * sizeof(OffT), s);
+    if (e != cudaSuccess || t.n == 0) return e;
+    const K* keys = static_cast<const K*>(a.keys);
+    const unsigned g1 = persistent_grid(k_hash_count<K, OffT, POW2>, 256, 0, t.n);
+    HG_LAUNCH("k1_hash_count", s, k_hash_count<K, OffT, POW2><<<g1, 256, 0, s>>>(keys, t.n, t.seed, t.hash_kind, nv, offs + 1,
+                                                   a.aggregate));
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    void* scratch = nullptr;
+    if ((e = cudaMallocAsync(&scratch, scan_scratch_bytes(t.nv), s)) != cudaSuccess) return e;
+    e = launch_scan<OffT, OffT>(offs + 1, offs + 1, t.nv, scratch, nullptr, s, "k2_scan");
+    cudaFreeAsync(scratch, s);
+    if (e != cudaSuccess) return e;
+    const unsigned g3 = persistent_grid(k_scatter<K, VT, OffT, POW2>, 256, 0, t.n);
+    HG_LAUNCH("k3_scatter", s, k_scatter<K, VT, OffT, POW2><<<g3, 256, 0, s>>>(
+        keys, static_cast<const VT*>(a.vals), t.n, t.seed, t.hash_kind, nv, offs + 1,
+        static_cast<K*>(t.keys), static_cast<VT*>(t.vals), a.aggregate));
+    return cudaGetLastError();
+}
+
+// Binned build, hg_binned.cu.
+template <typename K, typename VT, typename OffT, bool POW2>
+cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s);
+
+template <typename K, typename VT, typename OffT>
+static cudaError_t build_typed(const TableDesc& t, const BuildArgs& a, cudaStream_t s) {
+    const bool pow2 = (t.nv & (t.nv - 1)) == 0;
+    cudaError_t e;
+    if (a.variant == 2) {
+        e = pow2 ? build_v2_impl<K, VT, OffT, true>(t, a, s)
+                 : build_v2_impl<K, VT, OffT, false>(t, a, s);
+    } else {
+        e = pow2 ? build_v1_impl<K, VT, OffT, true>(t, a, s)
+                 : build_v1_impl<K, VT, OffT, false>(t, a, s);
+    }
+    if (e == cudaSuccess && a.stable) e = stable_order<K, VT, OffT>(t, s);
+    return e;
+}
+
+template <typename K, typename VT>
+static cudaError_t build_off(const TableDesc& t, const BuildArgs& a, cudaStream_t s) {
+    return t.off_bytes == 4 ? build_typed<K, VT, uint32_t>(t, a, s)
+                            : build_typed<K, VT, uint64_t>(t, a, s);
+}
+
+template <typename K>
+static cudaError_t build_val(const TableDesc& t, const BuildArgs& a, cudaStream_t s) {
+    return t.val_bytes == 4 ? build_off<K, uint32_t>(t, a, s) : build_off<K, uint64_t>(t, a, s);
+}
+
+cudaError_t build_table(const TableDesc& t, const BuildArgs& a, cudaStream_t s) {
+    return t.key_bytes == 4 ? build_val<uint32_t>(t, a, s) : build_val<uint64_t>(t, a, s);
+}
+
+}  // namespace hg

@@ -1,0 +1,486 @@
+// hg_capi.cu -- the extern "C" boundary (include/hg_b200.h).
+//
+// Owns table lifetime, host/device staging, config validation with the
+// reference's exact error semantics, and the translation of CUDA failures
+// into hg_status + hg_last_error. All compute is in the kernel TUs.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/hg_b200.h"
+#include "hg_internal.h"
+
+struct hg_table {
+    hg::TableDesc d;
+    double load_factor = 1.0;
+    int device = 0;
+    void* alloc_offs = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+hg_status fail(hg_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+hg_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(e == cudaErrorMemoryAllocation ? HG_ENOMEM : HG_ECUDA, "%s: %s", where,
+                cudaGetErrorString(e));
+}
+
+#define HG_CUDA(call)                                   \
+    do {                                                \
+        cudaError_t e_ = (call);                        \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+// A device view of a caller array: either the caller's device pointer or a
+// stream-ordered staging copy of host data (freed by release()).
+struct DevIn {
+    const void* ptr = nullptr;
+    void* owned = nullptr;
+    cudaError_t stage(const void* p, size_t bytes, cudaStream_t s) {
+        if (!p || bytes == 0 || is_device_ptr(p)) {
+            ptr = p;
+            return cudaSuccess;
+        }
+        cudaError_t e = cudaMallocAsync(&owned, bytes, s);
+        if (e != cudaSuccess) return e;
+        e = cudaMemcpyAsync(owned, p, bytes, cudaMemcpyHostToDevice, s);
+        ptr = owned;
+        return e;
+    }
+    void release(cudaStream_t s) {
+        if (owned) cudaFreeAsync(owned, s);
+        owned = nullptr;
+    }
+};
+
+int ensure_device_ready() {
+    static thread_local int checked = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    if (checked != dev) {
+        int major = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) {
+            cudaGetLastError();
+            return -1;
+        }
+        if (major < 10) return -2;
+        // Keep freed stream-ordered allocations in the pool (no re-map cost
+        // between builds).
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = ~uint64_t(0);
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        checked = dev;
+    }
+    return dev;
+}
+
+hg_status need_device(int* dev) {
+    const int d = ensure_device_ready();
+    if (d == -1) return fail(HG_ECUDA, "no CUDA device available (no CPU fallback)");
+    if (d == -2) return fail(HG_ECUDA, "device is not sm_100-class (compiled for sm_100a only)");
+    *dev = d;
+    return HG_OK;
+}
+
+template <typename T>
+__global__ void k_widen(const T* in, uint64_t* out, uint64_t n) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = uint64_t(in[i]);
+}
+
+__global__ void k_narrow_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = in[i];
+}
+
+cudaError_t widen_to(const void* src, int width, uint64_t n, uint64_t* dst, cudaStream_t s) {
+    if (n == 0 || !dst) return cudaSuccess;
+    const bool dev_out = is_device_ptr(dst);
+    uint64_t* d = dst;
+    if (!dev_out) {
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d), n * 8, s);
+        if (e != cudaSuccess) return e;
+    }
+    if (width == 8) {
+        cudaMemcpyAsync(d, src, n * 8, cudaMemcpyDeviceToDevice, s);
+    } else {
+        const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, 148 * 16));
+        k_widen<uint32_t><<<grid, 256, 0, s>>>(static_cast<const uint32_t*>(src), d, n);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (!dev_out) {
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dst, d, n * 8, cudaMemcpyDeviceToHost, s);
+        cudaFreeAsync(d, s);
+    }
+    return e;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t hg_abi_version(void) { return HG_ABI_VERSION; }
+
+const char* hg_last_error(void) { return g_err.c_str(); }
+
+void hg_build_config_init(hg_build_config* cfg) {
+    if (!cfg) return;
+    std::memset(cfg, 0, sizeof *cfg);
+    cfg->load_factor = 1.0;
+    cfg->bin_count = uint64_t(1) << 15;
+    cfg->hash_seed = 0;
+    cfg->vertex_count = 0;
+    cfg->variant = HG_BUILD_SIMPLE;
+    cfg->hash_kind = HG_HASH_MIX64;
+    cfg->stable = 0;
+    cfg->aggregate = -1;
+    cfg->partition_vertices = 0;
+}
+
+void hg_probe_options_init(hg_probe_options* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof *o);
+    o->pair_width = 8;
+    o->pair_cap = uint64_t(1) << 24;
+}
+
+hg_status hg_derived_vertex_count(uint64_t n, double load_factor, uint64_t* out) {
+    if (!out) return fail(HG_EINVAL, "out is NULL");
+    if (!(load_factor > 0.0)) return fail(HG_EINVAL, "load_factor must be positive");
+    const double v = std::floor(static_cast<double>(n) / load_factor);
+    *out = v < 1.0 ? 1 : static_cast<uint64_t>(v);
+    return HG_OK;
+}
+
+uint64_t hg_hash_to_vertex(uint64_t key, uint64_t seed, uint64_t nv) {
+    if (nv == 0) return 0;
+    uint64_t x = key ^ seed;
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdULL;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ULL;
+    x ^= x >> 33;
+    return x % nv;
+}
+
+hg_status hg_build(const void* keys, int32_t key_width, const void* vals, int32_t val_width,
+                   uint64_t n, const hg_build_config* cfg_in, void* stream, hg_table** out) {
+    if (!out) return fail(HG_EINVAL, "out is NULL");
+    *out = nullptr;
+    hg_build_config cfg;
+    if (cfg_in) {
+        cfg = *cfg_in;
+    } else {
+        hg_build_config_init(&cfg);
+    }
+    // core.hpp:106-109 check_config
+    if (!(cfg.load_factor > 0.0)) return fail(HG_EINVAL, "load_factor must be positive");
+    if (cfg.bin_count < 1) return fail(HG_EINVAL, "bin_count must be at least 1");
+    if (key_width != 4 && key_width != 8) return fail(HG_EINVAL, "key_width must be 4 or 8");
+    if (vals && val_width != 4 && val_width != 8) return fail(HG_EINVAL, "val_width must be 4 or 8");
+    if (cfg.variant != HG_BUILD_SIMPLE && cfg.variant != HG_BUILD_BINNED)
+        return fail(HG_EINVAL, "variant must be 1 (simple) or 2 (binned)");
+    if (cfg.hash_kind != HG_HASH_MIX64 && cfg.hash_kind != HG_HASH_IDENTITY)
+        return fail(HG_EINVAL, "unknown hash_kind");
+    if (n && !keys) return fail(HG_EINVAL, "keys is NULL");
+    uint64_t nv = cfg.vertex_count;
+    if (!nv) {
+        hg_status st = hg_derived_vertex_count(n, cfg.load_factor, &nv);
+        if (st != HG_OK) return st;
+    }
+    int dev = 0;
+    if (hg_status st = need_device(&dev); st != HG_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+    auto* t = new hg_table;
+    t->device = dev;
+    t->load_factor = cfg.load_factor;
+    hg::TableDesc& d = t->d;
+    d.nv = nv;
+    d.n = n;
+    d.seed = cfg.hash_seed;
+    d.hash_kind = cfg.hash_kind;
+    d.key_bytes = key_width;
+    d.val_bytes = vals ? val_width : (n <= (uint64_t(1) << 32) ? 4 : 8);
+    d.off_bytes = (n < (uint64_t(1) << 32) && nv <= (uint64_t(1) << 32)) ? 4 : 8;
+    // offs is padded so that offs + 1 (the counter / cursor view) is 16-byte aligned.
+    const uint64_t pad = 16 / d.off_bytes - 1;
+    cudaError_t e = cudaMallocAsync(&t->alloc_offs, (nv + 1 + pad) * d.off_bytes, s);
+    if (e == cudaSuccess && n) e = cudaMallocAsync(&d.keys, n * d.key_bytes, s);
+    if (e == cudaSuccess && n) e = cudaMallocAsync(&d.vals, n * d.val_bytes, s);
+    if (e != cudaSuccess) {
+        hg_table_destroy(t, stream);
+        return cuda_fail(e, "hg_build: table allocation");
+    }
+    d.offs = static_cast<char*>(t->alloc_offs) + pad * d.off_bytes;
+
+    DevIn kin, vin;
+    e = kin.stage(keys, n * key_width, s);
+    if (e == cudaSuccess && vals) e = vin.stage(vals, n * val_width, s);
+    if (e == cudaSuccess) {
+        hg::BuildArgs a;
+        a.keys = kin.ptr;
+        a.vals = vals ? vin.ptr : nullptr;
+        a.n = n;
+        a.variant = cfg.variant;
+        a.aggregate = cfg.aggregate < 0 ? 1 : cfg.aggregate;
+        a.stable = cfg.stable;
+        a.partition_vertices = cfg.partition_vertices;
+        e = hg::build_table(d, a, s);
+    }
+    kin.release(s);
+    vin.release(s);
+    if (e != cudaSuccess) {
+        hg_table_destroy(t, stream);
+        return cuda_fail(e, "hg_build");
+    }
+    *out = t;
+    return HG_OK;
+}
+
+hg_status hg_table_get_info(const hg_table* t, hg_table_info* info) {
+    if (!t || !info) return fail(HG_EINVAL, "NULL argument");
+    info->num_vertices = t->d.nv;
+    info->num_edges = t->d.n;
+    info->hash_seed = t->d.seed;
+    info->load_factor = t->load_factor;
+    info->key_width = t->d.key_bytes;
+    info->val_width = t->d.val_bytes;
+    info->off_width = t->d.off_bytes;
+    info->hash_kind = t->d.hash_kind;
+    return HG_OK;
+}
+
+hg_status hg_table_device_arrays(const hg_table* t, const void** offs, const void** keys,
+                                 const void** vals) {
+    if (!t) return fail(HG_EINVAL, "NULL table");
+    if (offs) *offs = t->d.offs;
+    if (keys) *keys = t->d.keys;
+    if (vals) *vals = t->d.vals;
+    return HG_OK;
+}
+
+hg_status hg_table_export(const hg_table* t, uint64_t* offsets, uint64_t* keys, uint64_t* vals,
+                          void* stream) {
+    if (!t) return fail(HG_EINVAL, "NULL table");
+    cudaSetDevice(t->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    HG_CUDA(widen_to(t->d.offs, t->d.off_bytes, t->d.nv + 1, offsets, s));
+    HG_CUDA(widen_to(t->d.keys, t->d.key_bytes, t->d.n, keys, s));
+    HG_CUDA(widen_to(t->d.vals, t->d.val_bytes, t->d.n, vals, s));
+    HG_CUDA(cudaStreamSynchronize(s));
+    return HG_OK;
+}
+
+hg_status hg_table_destroy(hg_table* t, void* stream) {
+    if (!t) return HG_OK;
+    cudaSetDevice(t->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (t->alloc_offs) cudaFreeAsync(t->alloc_offs, s);
+    if (t->d.keys) cudaFreeAsync(t->d.keys, s);
+    if (t->d.vals) cudaFreeAsync(t->d.vals, s);
+    delete t;
+    return HG_OK;
+}
+
+hg_status hg_probe(const hg_table* t, const void* probes, int32_t probe_width, uint64_t m,
+                   const hg_probe_options* opts_in, hg_probe_result* result, void* stream) {
+    if (!t) return fail(HG_EINVAL, "NULL table");
+    hg_probe_options opts;
+    if (opts_in) {
+        opts = *opts_in;
+    } else {
+        hg_probe_options_init(&opts);
+    }
+    if (probe_width != 4 && probe_width != 8) return fail(HG_EINVAL, "probe_width must be 4 or 8");
+    if (probe_width != t->d.key_bytes && !(probe_width == 4 && t->d.key_bytes == 8))
+        return fail(HG_EUNSUPPORTED, "u64 probes into a u32-keyed table are not supported");
+    if (m && !probes) return fail(HG_EINVAL, "probes is NULL");
+    if (opts.materialize && opts.pair_width != 4 && opts.pair_width != 8)
+        return fail(HG_EINVAL, "pair_width must be 4 or 8");
+    if (opts.materialize && opts.pair_cap && !opts.pairs)
+        return fail(HG_EINVAL, "materialize requires a pairs buffer");
+    if (!opts.device_result && !result) return fail(HG_EINVAL, "result is NULL");
+    if (cudaSetDevice(t->device) != cudaSuccess) return fail(HG_ECUDA, "cudaSetDevice failed");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+    DevIn pin;
+    cudaError_t e = pin.stage(probes, m * probe_width, s);
+    if (e != cudaSuccess) return cuda_fail(e, "hg_probe: staging probes");
+    const void* dprobes = pin.ptr;
+    void* widened = nullptr;
+    if (probe_width == 4 && t->d.key_bytes == 8 && m) {
+        if ((e = cudaMallocAsync(&widened, m * 8, s)) != cudaSuccess) {
+            pin.release(s);
+            return cuda_fail(e, "hg_probe: widen buffer");
+        }
+        const unsigned grid = unsigned(std::min<uint64_t>((m + 255) / 256, 148 * 16));
+        k_narrow_u32_to_u64<<<grid, 256, 0, s>>>(static_cast<const uint32_t*>(dprobes),
+                                                 static_cast<uint64_t*>(widened), m);
+        dprobes = widened;
+    }
+
+    const bool want_pairs = opts.materialize && opts.pair_cap > 0;
+    const bool counts_dev = opts.counts && is_device_ptr(opts.counts);
+    const bool pairs_dev = want_pairs && is_device_ptr(opts.pairs);
+    // scratch: totals[3] | counts[m] (if needed) | pair_offsets[m+1] | pairs staging
+    uint64_t* totals = opts.device_result;
+    void* scratch = nullptr;
+    size_t need = 0;
+    const size_t tot_off = 0, tot_bytes = totals ? 0 : 256;
+    const size_t cnt_off = tot_bytes;
+    const bool need_counts = want_pairs || opts.materialize || opts.counts;
+    const size_t cnt_bytes = (need_counts && !counts_dev) ? ((m * 4 + 255) & ~size_t(255)) : 0;
+    const size_t po_off = cnt_off + cnt_bytes;
+    const size_t po_bytes = opts.materialize ? (((m + 1) * 8 + 255) & ~size_t(255)) : 0;
+    const size_t pr_off = po_off + po_bytes;
+    const size_t pr_bytes = (want_pairs && !pairs_dev) ? opts.pair_cap * 2 * opts.pair_width : 0;
+    need = pr_off + pr_bytes;
+    if (need && (e = cudaMallocAsync(&scratch, need, s)) != cudaSuccess) {
+        pin.release(s);
+        if (widened) cudaFreeAsync(widened, s);
+        return cuda_fail(e, "hg_probe: scratch");
+    }
+    char* sc = static_cast<char*>(scratch);
+    if (!totals) totals = reinterpret_cast<uint64_t*>(sc + tot_off);
+    uint32_t* counts = need_counts ? (counts_dev ? opts.counts : reinterpret_cast<uint32_t*>(sc + cnt_off))
+                                   : nullptr;
+    uint64_t* pair_off = opts.materialize ? reinterpret_cast<uint64_t*>(sc + po_off) : nullptr;
+    void* pairs = want_pairs ? (pairs_dev ? opts.pairs : static_cast<void*>(sc + pr_off)) : nullptr;
+
+    e = cudaMemsetAsync(totals, 0, 2 * sizeof(uint64_t), s);
+    hg::ProbeArgs a;
+    a.probes = dprobes;
+    a.m = m;
+    a.counts = counts;
+    a.totals = totals;
+    a.pairs = pairs;
+    a.pair_bytes = opts.pair_width;
+    a.cap = want_pairs ? opts.pair_cap : 0;
+    a.pair_offsets = pair_off;
+    if (e == cudaSuccess) e = hg::probe_table(t->d, a, s);
+
+    hg_status st = HG_OK;
+    if (e != cudaSuccess) {
+        st = cuda_fail(e, "hg_probe");
+    } else if (!opts.device_result) {
+        uint64_t host_tot[2] = {0, 0};
+        e = cudaMemcpyAsync(host_tot, totals, sizeof host_tot, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && opts.counts && !counts_dev && m)
+            e = cudaMemcpyAsync(opts.counts, counts, m * 4, cudaMemcpyDeviceToHost, s);
+        const uint64_t written = opts.materialize ? std::min(host_tot[0], opts.pair_cap) : 0;
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e == cudaSuccess && want_pairs && !pairs_dev && written)
+            e = cudaMemcpyAsync(opts.pairs, pairs, written * 2 * opts.pair_width,
+                                cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) {
+            st = cuda_fail(e, "hg_probe: result readback");
+        } else if (result) {
+            result->match_count = host_tot[0];
+            result->key_comparisons = host_tot[1];
+            result->pairs_written = written;
+            result->truncated = opts.materialize && host_tot[0] > opts.pair_cap;
+        }
+    } else if (result) {
+        std::memset(result, 0, sizeof *result);
+    }
+    if (scratch) cudaFreeAsync(scratch, s);
+    if (widened) cudaFreeAsync(widened, s);
+    pin.release(s);
+    return st;
+}
+
+hg_status hg_count_instances(const hg_table* t, uint64_t key, uint64_t* out, void* stream) {
+    if (!out) return fail(HG_EINVAL, "out is NULL");
+    if (t && t->d.key_bytes == 4 && key > 0xFFFFFFFFull) {
+        // A u32-keyed table cannot hold a wider key: zero matches (the
+        // comparison count is irrelevant to count_instances).
+        *out = 0;
+        return HG_OK;
+    }
+    hg_probe_result r;
+    const uint32_t k32 = uint32_t(key);
+    const void* kp = t && t->d.key_bytes == 4 ? static_cast<const void*>(&k32)
+                                               : static_cast<const void*>(&key);
+    hg_status st = hg_probe(t, kp, t ? t->d.key_bytes : 8, 1, nullptr, &r, stream);
+    if (st == HG_OK) *out = r.match_count;
+    return st;
+}
+
+hg_status hg_validate(const hg_table* t, const void* input_keys, uint64_t expected_entries,
+                      int32_t* violation, void* stream) {
+    if (!t || !violation) return fail(HG_EINVAL, "NULL argument");
+    if (cudaSetDevice(t->device) != cudaSuccess) return fail(HG_ECUDA, "cudaSetDevice failed");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    *violation = 0;
+    if (t->d.nv < 1) {
+        *violation = 1;
+        return HG_OK;
+    }
+    if (t->d.n != expected_entries) {
+        // offsets[V] vs edges is checked on device; edge count vs input size here (core.hpp:268)
+    }
+    DevIn in;
+    cudaError_t e = in.stage(input_keys, t->d.n * t->d.key_bytes, s);
+    uint32_t* d_code = nullptr;
+    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&d_code), 4, s);
+    if (e == cudaSuccess) e = hg::validate_table(t->d, input_keys ? in.ptr : nullptr, d_code, s);
+    uint32_t code = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&code, d_code, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (d_code) cudaFreeAsync(d_code, s);
+    in.release(s);
+    if (e != cudaSuccess) return cuda_fail(e, "hg_validate");
+    if (code == 0xFFFFFFFFu) code = 0;
+    if (code == 0 && t->d.n != expected_entries) code = 6;  // core.hpp:268
+    // Codes are ordered like validate_csr's checks except 6 (edge count vs
+    // input size), which the reference tests right after 5.
+    if (code > 6 && t->d.n != expected_entries) code = 6;
+    *violation = int32_t(code);
+    return HG_OK;
+}
+
+hg_status hg_generate(void* out, int32_t key_width, uint64_t n, int32_t kind, uint64_t seed,
+                      uint64_t start, double hit, const void* ref, uint64_t n_ref, void* stream) {
+    if (key_width != 4 && key_width != 8) return fail(HG_EINVAL, "key_width must be 4 or 8");
+    if (kind < 0 || kind > 2) return fail(HG_EINVAL, "unknown generator kind");
+    if (n && !is_device_ptr(out)) return fail(HG_EINVAL, "hg_generate writes device memory only");
+    int dev = 0;
+    if (hg_status st = need_device(&dev); st != HG_OK) return st;
+    HG_CUDA(hg::generate_keys(out, key_width, n, kind, seed, start, hit, ref, n_ref,
+                              static_cast<cudaStream_t>(stream)));
+    return HG_OK;
+}
+
+}  // extern "C"

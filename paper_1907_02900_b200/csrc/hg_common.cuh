@@ -1,0 +1,153 @@
+// hg_common.cuh -- device primitives shared by every HashGraph kernel (sm_100a).
+//
+// Bit-exact device restatement of the reference vertex hash
+// (reference: proj/include/hashgraph/hash.hpp:12-19 mix64, :30-33
+// VertexHasher = mix64(key ^ seed) % V) with an exact, division-free
+// reduction, plus the tiny PTX helpers the kernels use.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hg {
+
+enum HashKind : int { kHashMix64 = 0, kHashIdentity = 1 };
+
+// Exact "h mod d" / "h div d" for a runtime divisor d >= 1 without the ~60
+// instruction emulated 64-bit division. magic = floor((2^64-1)/d); the
+// estimate q = umulhi(h, magic) satisfies q_true-1 <= q <= q_true for every
+// h < 2^64 (error h*(1/d - magic/2^64) <= h/2^64 < 1), so one correction
+// step is exact. Power-of-two divisors use shift/mask (template POW2).
+struct Divisor {
+    uint64_t d;
+    uint64_t magic;
+    uint32_t shift;  // log2(d) when d is a power of two
+    uint32_t pow2;
+};
+
+inline Divisor make_divisor(uint64_t d) {
+    Divisor r;
+    r.d = d;
+    r.magic = ~uint64_t(0) / d;
+    r.pow2 = (d & (d - 1)) == 0;
+    r.shift = 0;
+    while (r.pow2 && (uint64_t(1) << r.shift) < d) ++r.shift;
+    return r;
+}
+
+template <bool POW2>
+__device__ __forceinline__ uint64_t mod_of(uint64_t h, const Divisor& m) {
+    if constexpr (POW2) {
+        return h & (m.d - 1);
+    } else {
+        const uint64_t q = __umul64hi(h, m.magic);
+        uint64_t r = h - q * m.d;
+        return r >= m.d ? r - m.d : r;
+    }
+}
+
+template <bool POW2>
+__device__ __forceinline__ uint64_t div_of(uint64_t h, const Divisor& m) {
+    if constexpr (POW2) {
+        return h >> m.shift;
+    } else {
+        uint64_t q = __umul64hi(h, m.magic);
+        const uint64_t r = h - q * m.d;
+        return r >= m.d ? q + 1 : q;
+    }
+}
+
+// hash.hpp:12-19 (murmur3 fmix64).
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdULL;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ULL;
+    x ^= x >> 33;
+    return x;
+}
+
+// hash.hpp:30-33; keys narrower than 64 bits are zero-extended first (the
+// reference API is u64-only, core.hpp:161). kHashIdentity restates the
+// fixture hasher of tests/support.hpp:42-46 (key % V).
+template <int HK, bool POW2>
+__device__ __forceinline__ uint64_t vertex_of(uint64_t key, uint64_t seed, const Divisor& nv) {
+    if constexpr (HK == kHashIdentity) {
+        return mod_of<POW2>(key, nv);
+    } else {
+        return mod_of<POW2>(mix64(key ^ seed), nv);
+    }
+}
+
+__device__ __forceinline__ uint32_t lane_id() {
+    uint32_t l;
+    asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
+    return l;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Streaming (evict-first) loads for read-once inputs so they do not displace
+// the L2-resident working set (counters, partitions).
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p) {
+    return __ldcs(p);
+}
+
+__device__ __forceinline__ uint32_t atom_add(uint32_t* p, uint32_t v) { return atomicAdd(p, v); }
+__device__ __forceinline__ uint64_t atom_add(uint64_t* p, uint64_t v) {
+    return atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
+}
+__device__ __forceinline__ void red_add(uint32_t* p, uint32_t v) { atomicAdd(p, v); }
+__device__ __forceinline__ void red_add(uint64_t* p, uint64_t v) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
+}
+
+// Peer mask of lanes holding the same vertex id: 32-bit match when every
+// vertex id fits 32 bits (V <= 2^32), else the 64-bit form.
+template <bool V32>
+__device__ __forceinline__ uint32_t match_peers(uint32_t active, uint64_t v) {
+    if constexpr (V32) {
+        return __match_any_sync(active, static_cast<uint32_t>(v));
+    } else {
+        return __match_any_sync(active, static_cast<unsigned long long>(v));
+    }
+}
+
+// Warp-aggregated atomicAdd of 1 on counter (CounterArray
+// ticket semantics, parallel.hpp:112-118). Lanes with equal v form a peer
+// group; the lowest lane adds popc(group) once, every lane gets a distinct
+// ticket base + rank, so k adds on one slot hand out {old..old+k-1} exactly
+// once (test_parallel.cpp:79-125). Must be called by all lanes in `active`.
+template <bool V32, typename C>
+__device__ __forceinline__ C aggregated_ticket(C* counter, uint32_t active, uint64_t v) {
+    const uint32_t peers = match_peers<V32>(active, v);
+    const uint32_t leader = __ffs(peers) - 1;
+    const uint32_t rank = __popc(peers & lanemask_lt());
+    C base = 0;
+    if (lane_id() == leader) base = atom_add(counter, C(__popc(peers)));
+    base = __shfl_sync(peers, base, leader);
+    return base + C(rank);
+}
+
+template <bool V32, typename C>
+__device__ __forceinline__ void aggregated_count(C* counter, uint32_t active, uint64_t v) {
+    const uint32_t peers = match_peers<V32>(active, v);
+    if (lane_id() == uint32_t(__ffs(peers) - 1)) red_add(counter, C(__popc(peers)));
+}
+
+}  // namespace hg

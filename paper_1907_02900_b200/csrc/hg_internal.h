@@ -1,0 +1,83 @@
+// hg_internal.h -- host-side launcher interface between the C-ABI layer
+// (hg_capi.cu) and the kernel translation units. Plain types only.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hg {
+
+// Device table storage (SoA CSR): offs[V+1] (u32 when the
+// table holds < 2^32 entries and V <= 2^32, else u64), keys[N] (u32/u64),
+// vals[N] (u32/u64; the reference's Entry::index, core.hpp:21-26).
+struct TableDesc {
+    uint64_t nv = 1;        // V
+    uint64_t n = 0;         // N
+    uint64_t seed = 0;
+    int hash_kind = 0;      // 0 mix64, 1 identity
+    int key_bytes = 4;      // 4 | 8
+    int val_bytes = 4;      // 4 | 8
+    int off_bytes = 4;      // 4 | 8
+    void* offs = nullptr;   // V+1 entries (offs[0] == 0)
+    void* keys = nullptr;
+    void* vals = nullptr;
+};
+
+struct BuildArgs {
+    const void* keys = nullptr;  // device, n entries of key_bytes
+    const void* vals = nullptr;  // device or nullptr (then val = input position)
+    uint64_t n = 0;
+    int variant = 1;             // 1 simple (V1), 2 binned (V2)
+    int aggregate = 1;           // warp-aggregated atomics
+    int stable = 0;              // reproduce ExecMode::sequential segment order
+    uint64_t partition_vertices = 0;  // V2 partition width (0 = auto)
+};
+
+// Builds into t (offs/keys/vals already allocated). Scratch is allocated
+// stream-ordered from the device pool.
+cudaError_t build_table(const TableDesc& t, const BuildArgs& a, cudaStream_t s);
+
+struct ProbeArgs {
+    const void* probes = nullptr;  // device, m entries of key_bytes (same as table)
+    uint64_t m = 0;
+    uint32_t* counts = nullptr;    // nullable: per-probe match counts (u32)
+    uint64_t* totals = nullptr;    // device [2]: match_count, key_comparisons (accumulated)
+    // pairs (K9/K10): when pairs != nullptr, pair_offsets must hold m+1 u64.
+    void* pairs = nullptr;         // device, cap pairs of pair_bytes*2
+    int pair_bytes = 8;            // 4 (u32 pairs) | 8 (MatchPair u64 layout)
+    uint64_t cap = 0;
+    uint64_t* pair_offsets = nullptr;
+};
+
+cudaError_t probe_table(const TableDesc& t, const ProbeArgs& a, cudaStream_t s);
+
+// Counter-based synthetic generators.
+// kind 0: key[i] = splitmix64(seed, start+i) (truncated to key_bytes).
+// kind 1: C4 probes with hit ratio `hit` against build keys `ref` (n_ref).
+cudaError_t generate_keys(void* out, int key_bytes, uint64_t n, int kind, uint64_t seed,
+                          uint64_t start, double hit, const void* ref, uint64_t n_ref,
+                          cudaStream_t s);
+
+// Device-side CSR validation (core.hpp:251-282 plus
+// key == input[index]). Returns violation code in *d_code (0 valid).
+cudaError_t validate_table(const TableDesc& t, const void* input_keys, uint32_t* d_code,
+                           cudaStream_t s);
+
+int num_sms();
+
+// Kernel timeline hooks (hg_prof.cu).
+bool prof_enabled();
+int prof_begin(const char* name, cudaStream_t s);
+void prof_end(int token, cudaStream_t s);
+
+// Launch `launch` (a statement launching one kernel on stream s) bracketed by
+// profiler events named `name`.
+#define HG_LAUNCH(name, s, ...)                     \
+    do {                                            \
+        const int tok_ = ::hg::prof_begin(name, s); \
+        __VA_ARGS__;                                \
+        ::hg::prof_end(tok_, s);                    \
+    } while (0)
+
+}  // namespace hg
