@@ -126,10 +126,14 @@ k_part_scatter(const K* __restrict__ keys, const VT* __restrict__ vals, uint64_t
 
 // ---------------------------------------------------------------- K7
 
-// Shared-memory layout per CTA: cnt[P] u32 | lv[cap] u16 | skeys[cap] | svals[cap]
+// Shared-memory layout per CTA (each region 16-byte aligned):
+//   cnt[P] u32 | lv[cap] u16 | skeys[cap] K | svals[cap] VT
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
 template <typename K, typename VT>
 __host__ __device__ constexpr size_t part_smem_bytes(uint32_t P, uint32_t cap) {
-    return size_t(P) * 4 + size_t(cap) * 2 + size_t(cap) * (sizeof(K) + sizeof(VT)) + 64;
+    return align16(size_t(P) * 4) + align16(size_t(cap) * 2) + align16(size_t(cap) * sizeof(K)) +
+           align16(size_t(cap) * sizeof(VT));
 }
 
 template <typename K, typename VT, typename OffT, bool POW2>
@@ -143,9 +147,9 @@ k_part_build(const typename PackedEntry<K, VT>::T* __restrict__ reorg,
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t P = 1u << pshift;
     uint32_t* cnt = reinterpret_cast<uint32_t*>(smem);
-    uint16_t* lvs = reinterpret_cast<uint16_t*>(cnt + P);
-    K* sk = reinterpret_cast<K*>(lvs + ((cap + 7) & ~7u));
-    VT* sv = reinterpret_cast<VT*>(sk + cap);
+    uint16_t* lvs = reinterpret_cast<uint16_t*>(smem + align16(size_t(P) * 4));
+    K* sk = reinterpret_cast<K*>(smem + align16(size_t(P) * 4) + align16(size_t(cap) * 2));
+    VT* sv = reinterpret_cast<VT*>(reinterpret_cast<unsigned char*>(sk) + align16(size_t(cap) * sizeof(K)));
     __shared__ uint32_t s_part;
     __shared__ uint32_t s_warp[16];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
@@ -253,7 +257,7 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     const size_t budget = std::min<size_t>(size_t(smem_optin) - 1024, 112 * 1024);
     auto cap_for = [&](uint32_t ps) -> uint32_t {
-        const size_t fixed = (size_t(1) << ps) * 4 + 64;
+        const size_t fixed = align16((size_t(1) << ps) * 4) + 64;
         if (budget <= fixed) return 0;
         return uint32_t((budget - fixed) / (2 + sizeof(K) + sizeof(VT))) & ~7u;
     };
