@@ -127,6 +127,8 @@ typedef struct hg_probe_options {
     uint32_t* counts;        /* nullable: per-probe match counts (count_instances per key) */
     uint64_t* device_result; /* nullable device u64[2] {match_count, key_comparisons}; when set
                                 the call is fully asynchronous (result is zeroed) */
+    int32_t method;          /* 0 auto, 1 direct gathers, 2 vertex-range partitioned probes */
+    int32_t reserved;
 } hg_probe_options;
 
 void hg_probe_options_init(hg_probe_options* opts);

@@ -54,6 +54,8 @@ class hg_probe_options(C.Structure):
         ("pairs", C.c_void_p),
         ("counts", C.c_void_p),
         ("device_result", C.c_void_p),
+        ("method", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 

@@ -388,6 +388,7 @@ hg_status hg_probe(const hg_table* t, const void* probes, int32_t probe_width, u
     a.pair_bytes = opts.pair_width;
     a.cap = want_pairs ? opts.pair_cap : 0;
     a.pair_offsets = pair_off;
+    a.method = opts.method;
     if (e == cudaSuccess) e = hg::probe_table(t->d, a, s);
 
     hg_status st = HG_OK;

@@ -108,6 +108,69 @@ __device__ __forceinline__ T ld_stream(const T* p) {
     return __ldcs(p);
 }
 
+// ---- TMA 1-D bulk copies + mbarriers (sm_90+ async proxy; SASS UBLKCP / SYNCS)
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+                 : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// Orders this thread's prior generic-proxy shared-memory accesses before
+// subsequent async-proxy (TMA) accesses to the same buffer.
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+// dst (shared) <- src (global), bytes % 16 == 0, both 16-byte aligned.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// Issues the 16-byte-aligned superset of global bytes [src, src + bytes) into
+// dst; returns the byte offset of src inside dst. Caller's buffer must hold
+// bytes + 32.
+__device__ __forceinline__ uint32_t tma_load_span(void* dst, const void* src, uint32_t bytes,
+                                                  uint64_t* bar) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+    const uintptr_t lo = a & ~uintptr_t(15);
+    const uintptr_t hi = (a + bytes + 15) & ~uintptr_t(15);
+    const uint32_t len = uint32_t(hi - lo);
+    mbar_arrive_expect_tx(bar, len);
+    if (len) tma_load_1d(dst, reinterpret_cast<const void*>(lo), len, bar);
+    return uint32_t(a - lo);
+}
+
 __device__ __forceinline__ uint32_t atom_add(uint32_t* p, uint32_t v) { return atomicAdd(p, v); }
 __device__ __forceinline__ uint64_t atom_add(uint64_t* p, uint64_t v) {
     return atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));

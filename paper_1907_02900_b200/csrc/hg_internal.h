@@ -48,6 +48,7 @@ struct ProbeArgs {
     int pair_bytes = 8;            // 4 (u32 pairs) | 8 (MatchPair u64 layout)
     uint64_t cap = 0;
     uint64_t* pair_offsets = nullptr;
+    int method = 0;                // 0 auto, 1 direct gathers, 2 partitioned
 };
 
 cudaError_t probe_table(const TableDesc& t, const ProbeArgs& a, cudaStream_t s);

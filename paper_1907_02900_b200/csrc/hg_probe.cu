@@ -11,10 +11,19 @@
 //                      slots, keeping slots < pair_cap (join.hpp:68-75)
 // Segments longer than kLongSeg are walked warp-cooperatively (the 32 lanes
 // stride one segment) so skewed, heavy vertices do not serialise one lane.
+//
+// Partitioned probe (large tables): a random probe costs two random HBM
+// sector reads (offsets, then keys), which caps the direct kernels at the
+// ~40 G random accesses/s of HBM (profiles/r01_microbench_b200.txt). When the
+// table is far larger than L2, the probes are first radix-partitioned by
+// vertex range with the build's machinery (hg_radix.cuh); k_probe_part then
+// stages one partition's offsets and keys slice in shared memory (coalesced)
+// and answers every probe of that partition from shared memory.
 #include <algorithm>
 
 #include "hg_common.cuh"
 #include "hg_internal.h"
+#include "hg_radix.cuh"
 #include "hg_scan.cuh"
 
 namespace hg {
@@ -207,6 +216,277 @@ k_probe_write(const K* __restrict__ probes, uint64_t m, uint64_t seed, int hk, D
     }
 }
 
+// ------------------------------------------------------------ partitioned
+
+constexpr int kPartProbeBlock = 512;
+
+// MODE 0: totals only; 1: totals + per-probe count at the probe's partitioned
+// position (pcount[pos]) or, with ORIG, at its original index; 2: pairs.
+template <typename K, typename VT, typename OffT, typename IT, bool POW2, int MODE, bool ORIG,
+          typename PT>
+__global__ void __launch_bounds__(kPartProbeBlock)
+k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __restrict__ ppart,
+             uint64_t nparts, uint64_t nv_total, uint64_t seed, int hk, Divisor nv,
+             uint32_t pshift, const OffT* __restrict__ offs, const K* __restrict__ tkeys,
+             const VT* __restrict__ tvals, uint32_t kcap, uint32_t* __restrict__ pcount,
+             const uint64_t* __restrict__ pair_off, void* __restrict__ pairs, uint64_t cap,
+             uint64_t* __restrict__ totals, uint32_t* ticket) {
+    using PE = EntryT<K, IT>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const uint32_t P = 1u << pshift;
+    uint32_t* soff = reinterpret_cast<uint32_t*>(smem);
+    K* skeys = reinterpret_cast<K*>(smem + ((size_t(P + 1) * 4 + 15) & ~size_t(15)));
+    __shared__ uint32_t s_part;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t nwarps = kPartProbeBlock / 32;
+    uint64_t matches = 0, compared = 0;
+    while (true) {
+        if (tid == 0) s_part = atomicAdd(ticket, 1u);
+        __syncthreads();
+        const uint64_t p = s_part;
+        if (p >= nparts) break;
+        const uint64_t vb = p << pshift;
+        const uint32_t pv = uint32_t(nv_total - vb < P ? nv_total - vb : uint64_t(P));
+        const uint64_t tb = offs[vb], te = offs[vb + pv];
+        const uint64_t tn = te - tb;
+        const bool staged = tn <= kcap;
+        // relative offsets fit u32 whenever the slice is staged; unstaged
+        // slices fall back to 64-bit global offsets below
+        for (uint32_t j = tid; j <= pv; j += kPartProbeBlock) soff[j] = uint32_t(uint64_t(offs[vb + j]) - tb);
+        if (staged)
+            for (uint64_t j = tid; j < tn; j += kPartProbeBlock) skeys[j] = tkeys[tb + j];
+        __syncthreads();
+        const K* kp = staged ? skeys : tkeys + tb;
+        const uint64_t q0 = ppart[p], q1 = ppart[p + 1];
+        const uint64_t qn = q1 - q0;
+        for (uint64_t base = uint64_t(warp) * 32; base < qn; base += uint64_t(nwarps) * 32) {
+            const uint64_t i = base + lane;
+            const bool valid = i < qn;
+            K key = 0;
+            typename std::conditional<std::is_void<IT>::value, uint32_t, IT>::type pidx = 0;
+            uint64_t b = 0, e = 0;
+            if (valid) {
+                const auto ent = pin[q0 + i];
+                key = PE::key(ent);
+                if constexpr (PE::kHasVal) pidx = PE::val(ent);
+                const uint32_t lv = uint32_t(hv<POW2>(key, seed, hk, nv) - vb);
+                if (staged) {
+                    b = soff[lv];
+                    e = soff[lv + 1];
+                } else {
+                    b = uint64_t(offs[vb + lv]) - tb;
+                    e = uint64_t(offs[vb + lv + 1]) - tb;
+                }
+            }
+            const uint64_t len = e - b;
+            compared += len;
+            uint32_t c = 0;
+            if (len <= kLongSeg)
+                for (uint64_t t = b; t < e; ++t) c += kp[t] == key;
+            uint32_t longm = __ballot_sync(0xffffffffu, len > kLongSeg);
+            while (longm) {
+                const int src = __ffs(longm) - 1;
+                longm &= longm - 1;
+                const uint64_t kb = __shfl_sync(0xffffffffu, b, src);
+                const uint64_t ke = __shfl_sync(0xffffffffu, e, src);
+                const K kk = __shfl_sync(0xffffffffu, key, src);
+                uint32_t cc = 0;
+                for (uint64_t t = kb + lane; t < ke; t += 32) cc += kp[t] == kk;
+                cc = warp_sum(cc);
+                if (int(lane) == src) c = cc;
+            }
+            matches += c;
+            if constexpr (MODE == 1) {
+                if (valid) {
+                    if constexpr (ORIG) pcount[pidx] = c;
+                    else pcount[q0 + i] = c;
+                }
+            }
+            if constexpr (MODE == 2) {
+                uint64_t sl = (valid && c) ? pair_off[q0 + i] : 0;
+                if (valid && c && len <= kLongSeg) {
+                    for (uint64_t t = b; t < e && sl < cap; ++t) {
+                        if (kp[t] == key) {
+                            store_pair<PT>(pairs, sl, uint64_t(tvals[tb + t]), uint64_t(pidx));
+                            ++sl;
+                        }
+                    }
+                }
+                uint32_t lm = __ballot_sync(0xffffffffu, valid && c && len > kLongSeg);
+                while (lm) {
+                    const int src = __ffs(lm) - 1;
+                    lm &= lm - 1;
+                    const uint64_t kb = __shfl_sync(0xffffffffu, b, src);
+                    const uint64_t ke = __shfl_sync(0xffffffffu, e, src);
+                    const K kk = __shfl_sync(0xffffffffu, key, src);
+                    uint64_t ws = __shfl_sync(0xffffffffu, sl, src);
+                    const uint64_t pj = __shfl_sync(0xffffffffu, uint64_t(pidx), src);
+                    for (uint64_t t0 = kb; t0 < ke && ws < cap; t0 += 32) {
+                        const uint64_t t = t0 + lane;
+                        const bool hit = t < ke && kp[t] == kk;
+                        const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+                        const uint64_t my = ws + __popc(hm & lanemask_lt());
+                        if (hit && my < cap) store_pair<PT>(pairs, my, uint64_t(tvals[tb + t]), pj);
+                        ws += __popc(hm);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    __shared__ unsigned long long s_m[kPartProbeBlock / 32], s_c[kPartProbeBlock / 32];
+    matches = warp_sum(matches);
+    compared = warp_sum(compared);
+    if (lane == 0) {
+        s_m[warp] = matches;
+        s_c[warp] = compared;
+    }
+    __syncthreads();
+    if (tid < 32) {
+        unsigned long long x = tid < nwarps ? s_m[tid] : 0, y = tid < nwarps ? s_c[tid] : 0;
+        x = warp_sum(x);
+        y = warp_sum(y);
+        if (tid == 0 && MODE != 2) {
+            if (x) atomicAdd(reinterpret_cast<unsigned long long*>(totals), x);
+            if (y) atomicAdd(reinterpret_cast<unsigned long long*>(totals + 1), y);
+        }
+    }
+}
+
+template <typename K, typename IT>
+__global__ void k_scatter_counts(const typename EntryT<K, IT>::T* __restrict__ pin,
+                                 const uint32_t* __restrict__ pcount, uint64_t m,
+                                 uint32_t* __restrict__ counts) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride)
+        counts[EntryT<K, IT>::val(pin[i])] = pcount[i];
+}
+
+template <typename K, typename VT, typename OffT, typename IT, bool POW2>
+static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cudaStream_t s) {
+    const Divisor nv = make_divisor(t.nv);
+    const OffT* offs = static_cast<const OffT*>(t.offs);
+    const K* tkeys = static_cast<const K*>(t.keys);
+    const VT* tvals = static_cast<const VT*>(t.vals);
+    const K* probes = static_cast<const K*>(a.probes);
+    constexpr uint32_t kTarget = 4096;
+    const PartGeom g = make_geom(t.nv, t.n, 0, double(kTarget));
+    const uint32_t P = 1u << g.pshift;
+    const uint32_t kcap = 3 * kTarget;
+    const size_t smem = ((size_t(P + 1) * 4 + 15) & ~size_t(15)) + size_t(kcap) * sizeof(K);
+    const bool need_idx = a.counts != nullptr || a.pairs != nullptr;
+    const int sms = num_sms();
+    cudaError_t e;
+    char* scratch = nullptr;
+    const size_t ps_bytes = ((g.nparts + 1) * sizeof(OffT) + 255) & ~size_t(255);
+    using E1 = typename EntryT<K, IT>::T;
+    using E0 = typename EntryT<K, void>::T;
+    const size_t ent = need_idx ? sizeof(E1) : sizeof(E0);
+    const size_t pscr = need_idx ? PartitionScratch<K, IT, OffT>::bytes(g, a.m)
+                                 : PartitionScratch<K, void, OffT>::bytes(g, a.m);
+    const size_t reorg_bytes = (a.m * ent + 255) & ~size_t(255);
+    const size_t cnt_bytes = a.pairs ? ((a.m * 4 + 255) & ~size_t(255)) : 0;
+    const size_t po_bytes = a.pairs ? (((a.m + 1) * 8 + 255) & ~size_t(255)) : 0;
+    const size_t scan_bytes = a.pairs ? ((scan_scratch_bytes(a.m) + 255) & ~size_t(255)) : 0;
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                             ps_bytes + pscr + reorg_bytes + cnt_bytes + po_bytes + scan_bytes + 256,
+                             s)) != cudaSuccess)
+        return e;
+    char* cur = scratch;
+    OffT* ppart = reinterpret_cast<OffT*>(cur);
+    cur += ps_bytes;
+    void* pscratch = cur;
+    cur += pscr;
+    void* reorg = cur;
+    cur += reorg_bytes;
+    uint32_t* pcount = reinterpret_cast<uint32_t*>(cur);
+    cur += cnt_bytes;
+    uint64_t* pair_off = reinterpret_cast<uint64_t*>(cur);
+    cur += po_bytes;
+    void* scan_scr = cur;
+    cur += scan_bytes;
+    uint32_t* ticket = reinterpret_cast<uint32_t*>(cur);
+    do {
+        if (need_idx) {
+            e = partition<K, IT, OffT, POW2>(probes, static_cast<const IT*>(nullptr), a.m, t.seed,
+                                             t.hash_kind, nv, g, ppart, pscratch,
+                                             static_cast<E1*>(reorg), s, "p_part_hist");
+        } else {
+            e = partition<K, void, OffT, POW2>(probes, static_cast<const void*>(nullptr), a.m,
+                                               t.seed, t.hash_kind, nv, g, ppart, pscratch,
+                                               static_cast<E0*>(reorg), s, "p_part_hist");
+        }
+        if (e != cudaSuccess) break;
+        auto launch = [&](auto kern, const char* name, uint32_t* pc, const uint64_t* po, void* pr,
+                          uint64_t cap) -> cudaError_t {
+            cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 int(smem));
+            if (r != cudaSuccess) return r;
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPartProbeBlock, smem);
+            const unsigned gk = unsigned(
+                std::min<uint64_t>(uint64_t(std::max(1, per_sm)) * sms, g.nparts));
+            if ((r = cudaMemsetAsync(ticket, 0, 4, s)) != cudaSuccess) return r;
+            HG_LAUNCH(name, s,
+                      kern<<<gk, kPartProbeBlock, smem, s>>>(
+                          static_cast<const E1*>(reorg), ppart, g.nparts, t.nv, t.seed,
+                          t.hash_kind, nv, g.pshift, offs, tkeys, tvals, kcap, pc, po, pr, cap,
+                          a.totals, ticket));
+            return cudaGetLastError();
+        };
+        if (!need_idx) {
+            // count-only: key-only entries
+            auto kern = k_probe_part<K, VT, OffT, void, POW2, 0, false, uint32_t>;
+            cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 int(smem));
+            if (r != cudaSuccess) { e = r; break; }
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPartProbeBlock, smem);
+            const unsigned gk = unsigned(
+                std::min<uint64_t>(uint64_t(std::max(1, per_sm)) * sms, g.nparts));
+            if ((e = cudaMemsetAsync(ticket, 0, 4, s)) != cudaSuccess) break;
+            HG_LAUNCH("k8p_probe_part", s,
+                      kern<<<gk, kPartProbeBlock, smem, s>>>(
+                          static_cast<const E0*>(reorg), ppart, g.nparts, t.nv, t.seed,
+                          t.hash_kind, nv, g.pshift, offs, tkeys, tvals, kcap, nullptr, nullptr,
+                          nullptr, 0, a.totals, ticket));
+            e = cudaGetLastError();
+            break;
+        }
+        if (!a.pairs) {
+            // per-probe counts in the caller's (original) order
+            e = launch(k_probe_part<K, VT, OffT, IT, POW2, 1, true, uint32_t>, "k8p_probe_part",
+                       a.counts, nullptr, nullptr, 0);
+            break;
+        }
+        // pairs: counts in partition order -> pair slots -> pairs
+        e = launch(k_probe_part<K, VT, OffT, IT, POW2, 1, false, uint32_t>, "k8p_probe_part",
+                   pcount, nullptr, nullptr, 0);
+        if (e != cudaSuccess) break;
+        if (a.counts) {
+            HG_LAUNCH("p_counts_scatter", s,
+                      (k_scatter_counts<K, IT><<<unsigned(std::min<uint64_t>((a.m + 255) / 256,
+                                                                             uint64_t(sms) * 16)),
+                                                 256, 0, s>>>(static_cast<const E1*>(reorg),
+                                                              pcount, a.m, a.counts)));
+            if ((e = cudaGetLastError()) != cudaSuccess) break;
+        }
+        if ((e = launch_scan<uint32_t, uint64_t>(pcount, pair_off, a.m, scan_scr, pair_off + a.m, s,
+                                                 "k9_pair_scan")) != cudaSuccess)
+            break;
+        if (a.cap == 0) break;
+        if (a.pair_bytes == 4) {
+            e = launch(k_probe_part<K, VT, OffT, IT, POW2, 2, false, uint32_t>, "k10p_probe_write",
+                       nullptr, pair_off, a.pairs, a.cap);
+        } else {
+            e = launch(k_probe_part<K, VT, OffT, IT, POW2, 2, false, uint64_t>, "k10p_probe_write",
+                       nullptr, pair_off, a.pairs, a.cap);
+        }
+    } while (false);
+    cudaFreeAsync(scratch, s);
+    return e;
+}
+
 template <typename K, typename VT, typename OffT, bool POW2>
 static cudaError_t probe_impl(const TableDesc& t, const ProbeArgs& a, cudaStream_t s) {
     const Divisor nv = make_divisor(t.nv);
@@ -216,6 +496,14 @@ static cudaError_t probe_impl(const TableDesc& t, const ProbeArgs& a, cudaStream
     if (a.m == 0) {
         if (a.pairs && a.pair_offsets) return cudaMemsetAsync(a.pair_offsets, 0, 8, s);
         return cudaSuccess;
+    }
+    const uint64_t table_bytes = (t.nv + 1) * sizeof(OffT) + t.n * sizeof(K);
+    const bool part = a.method == 2 || (a.method == 0 && table_bytes > (uint64_t(96) << 20) &&
+                                        a.m >= (uint64_t(1) << 20));
+    if (part) {
+        if (a.m <= (uint64_t(1) << 32))
+            return probe_partitioned<K, VT, OffT, uint32_t, POW2>(t, a, s);
+        return probe_partitioned<K, VT, OffT, uint64_t, POW2>(t, a, s);
     }
     const int sms = num_sms();
     const bool need_counts = a.counts != nullptr;

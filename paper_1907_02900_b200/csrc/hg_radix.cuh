@@ -1,0 +1,472 @@
+// hg_radix.cuh -- vertex-range partitioning machinery shared by the binned
+// build (V2) and the partitioned probe.
+//
+// The reference's V2 scatters entries into bins of consecutive vertex ranges
+// (core.hpp:192-219) so that the per-vertex passes run cache-resident. On
+// B200 the per-partition work runs in shared memory, which needs partitions
+// of ~2^12 vertices -- 2^16 partitions at V = 2^28. A one-shot 65536-way
+// scatter costs one global atomic and one uncoalesced store per key (measured
+// 7.4 ms at 2^28). Instead, partition ids are split into two <= 8-bit digits
+// and the entries go through two radix passes whose per-tile ranking runs on
+// shared-memory atomics (~1.8 T op/s on B200 vs ~0.13 T op/s for L2
+// atomics, profiles/r01_microbench_b200.txt):
+//
+//   k_part_hist    one pass over the keys; full 2^b partition histogram in
+//                  shared memory (two 16-bit halves per word, spilled to the
+//                  global histogram every 2^15 increments, so skew cannot
+//                  overflow); one global add per (CTA, non-empty partition)
+//   scan           exclusive scan of the histogram -> partition starts
+//   k_multisplit   per 4096-entry tile: shared-memory rank by digit, one global
+//                  atomic per (tile, digit) reserving a contiguous run, then
+//                  the tile is written digit-sorted, so stores coalesce into
+//                  runs of ~tile/256 entries. Pass 1 splits by the high digit
+//                  (reads the raw keys), pass 2 by the low digit within each
+//                  high-digit bucket (tiles never straddle a bucket).
+#pragma once
+
+#include <algorithm>
+#include <type_traits>
+
+#include "hg_common.cuh"
+#include "hg_internal.h"
+#include "hg_scan.cuh"
+
+namespace hg {
+
+int num_sms();
+
+// ------------------------------------------------------------ entry types
+// An entry is what travels through the passes: (key, value) for the build
+// and for probes that need their position; the bare key for count-only probes.
+template <typename K, typename VT>
+struct EntryT {
+    using T = ulonglong2;
+    static constexpr bool kHasVal = true;
+    __device__ static T make(K k, VT v) { return make_ulonglong2(k, v); }
+    __device__ static K key(const T& e) { return K(e.x); }
+    __device__ static VT val(const T& e) { return VT(e.y); }
+};
+template <>
+struct EntryT<uint32_t, uint32_t> {
+    using T = uint2;
+    static constexpr bool kHasVal = true;
+    __device__ static T make(uint32_t k, uint32_t v) { return make_uint2(k, v); }
+    __device__ static uint32_t key(const T& e) { return e.x; }
+    __device__ static uint32_t val(const T& e) { return e.y; }
+};
+template <typename K>
+struct EntryT<K, void> {
+    using T = K;
+    static constexpr bool kHasVal = false;
+    __device__ static T make(K k, uint64_t) { return k; }
+    __device__ static K key(const T& e) { return e; }
+    __device__ static uint32_t val(const T&) { return 0; }
+};
+
+template <bool POW2>
+__device__ __forceinline__ uint64_t hv(uint64_t key, uint64_t seed, int hk, const Divisor& nv) {
+    return hk == kHashIdentity ? vertex_of<kHashIdentity, POW2>(key, seed, nv)
+                               : vertex_of<kHashMix64, POW2>(key, seed, nv);
+}
+
+// ------------------------------------------------------------ geometry
+
+struct PartGeom {
+    uint32_t pshift = 0;  // partition width P = 2^pshift vertices
+    uint64_t nparts = 1;  // ceil(V / P) <= 2^16
+    uint32_t bits = 0;    // ceil(log2(nparts))
+    uint32_t b1 = 0, b2 = 0;  // digit widths (pass 1 high, pass 2 low), b1 + b2 = bits
+};
+
+inline uint32_t ceil_log2(uint64_t x) {
+    uint32_t b = 0;
+    while ((uint64_t(1) << b) < x) ++b;
+    return b;
+}
+
+// Partition width: aim for ~target entries per partition (N/V * P), never
+// more than 2^16 partitions (two 8-bit digits), never wider than 2^16.
+inline PartGeom make_geom(uint64_t nv, uint64_t n, uint64_t want_pv, double target) {
+    PartGeom g;
+    const uint32_t vbits = ceil_log2(nv);
+    uint32_t ps;
+    if (want_pv) {
+        ps = ceil_log2(want_pv);
+    } else {
+        const double per_vertex = n ? double(n) / double(nv) : 1.0;
+        ps = 0;
+        while (ps < 16 && per_vertex * double(uint64_t(2) << ps) <= target) ++ps;
+    }
+    if (vbits > 16 && ps < vbits - 16) ps = vbits - 16;
+    if (ps > 16) ps = 16;
+    if (ps > vbits) ps = vbits;
+    g.pshift = ps;
+    g.nparts = (nv + (uint64_t(1) << ps) - 1) >> ps;
+    g.bits = ceil_log2(g.nparts);
+    g.b2 = g.bits / 2;
+    g.b1 = g.bits - g.b2;
+    return g;
+}
+
+// ------------------------------------------------------------ histogram
+
+constexpr int kHistBlock = 1024;
+
+template <typename K, typename OffT, bool POW2>
+__global__ void __launch_bounds__(kHistBlock)
+k_part_hist(const K* __restrict__ keys, uint64_t n, uint64_t seed, int hk, Divisor nv,
+            uint32_t pshift, uint32_t nparts, OffT* __restrict__ hist) {
+    extern __shared__ uint32_t sh[];  // nparts/2 words, two 16-bit counters each
+    const uint32_t words = (nparts + 1) >> 1;
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    constexpr int VEC = 16 / sizeof(K);
+    using V = typename std::conditional<sizeof(K) == 4, uint4, ulonglong2>::type;
+    auto count = [&](K key) {
+        const uint32_t p = uint32_t(hv<POW2>(key, seed, hk, nv) >> pshift);
+        const uint32_t sft = (p & 1) << 4;
+        const uint32_t old = atomicAdd(sh + (p >> 1), 1u << sft);
+        if (((old >> sft) & 0xFFFFu) == 0x7FFFu) {
+            // this increment crossed 2^15: move 2^15 to the global count
+            atomicSub(sh + (p >> 1), 0x8000u << sft);
+            red_add(hist + p, OffT(0x8000));
+        }
+    };
+    uint64_t head = ((16 - (reinterpret_cast<uintptr_t>(keys) & 15)) & 15) / sizeof(K);
+    if (head > n) head = n;
+    const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (gtid < head) count(keys[gtid]);
+    const uint64_t nvec = (n - head) / VEC;
+    const V* body = reinterpret_cast<const V*>(keys + head);
+    uint64_t q = gtid;
+    for (; q + stride < nvec; q += 2 * stride) {
+        const V a = __ldcs(body + q);
+        const V b = __ldcs(body + q + stride);
+        const K* ka = reinterpret_cast<const K*>(&a);
+        const K* kb = reinterpret_cast<const K*>(&b);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) count(ka[k]);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) count(kb[k]);
+    }
+    if (q < nvec) {
+        const V a = __ldcs(body + q);
+        const K* ka = reinterpret_cast<const K*>(&a);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) count(ka[k]);
+    }
+    const uint64_t done = head + nvec * VEC;
+    if (gtid < n - done) count(keys[done + gtid]);
+    __syncthreads();
+    for (uint32_t p = threadIdx.x; p < nparts; p += blockDim.x) {
+        const uint32_t c = (sh[p >> 1] >> ((p & 1) << 4)) & 0xFFFFu;
+        if (c) red_add(hist + p, OffT(c));
+    }
+}
+
+// ------------------------------------------------------------ multisplit
+
+constexpr int kSplitBlock = 512;
+constexpr int kMaxDigits = 256;
+// 4096-entry tiles for <= 8-byte entries, 2048 for 16-byte ones (32 KB of
+// staging either way, so the kernel keeps 3-4 CTAs per SM).
+template <typename E>
+__host__ __device__ constexpr int split_items() { return sizeof(E) >= 16 ? 4 : 8; }
+template <typename E>
+__host__ __device__ constexpr int split_tile() { return kSplitBlock * split_items<E>(); }
+
+// One radix pass. RAW: input is the raw key array (+ optional vals, else the
+// input position is the value). Otherwise input is an entry array.
+// Digit of an entry = (p >> dshift) & dmask with p = partition id; the run
+// for digit d of a tile is reserved on cursor[cbase(tile) + d], where cbase is
+// 0 for pass 1 and (bucket << b2) for pass 2.
+// PASS2: tiles are laid out bucket by bucket; tile_prefix[b] = first tile of
+// high-digit bucket b (nb1 + 1 entries), bucket b spans
+// [part_start[b << b2], part_start[(b+1) << b2]).
+// Input tiles are double-buffered in shared memory with TMA 1-D bulk copies
+// (cp.async.bulk + mbarrier): tile i+1 streams in while tile i is ranked and
+// written, so HBM latency is off the critical path.
+template <typename K, typename VT, bool RAW>
+struct SplitLayout {
+    using E = typename EntryT<K, VT>::T;
+    using InT = typename std::conditional<RAW, K, E>::type;
+    static constexpr int kItems = split_items<E>();
+    static constexpr int kTile = split_tile<E>();
+    static constexpr size_t kInBytes = (size_t(kTile) * sizeof(InT) + 32 + 15) & ~size_t(15);
+    static constexpr size_t kBytes = 2 * kInBytes + size_t(kTile) * sizeof(E) + kTile;
+};
+
+template <typename K, typename VT, typename OffT, bool RAW, bool PASS2, bool POW2>
+__global__ void __launch_bounds__(kSplitBlock)
+k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t n, uint64_t seed,
+             int hk, Divisor nv, uint32_t pshift, uint32_t dshift, uint32_t dmask, uint32_t b2,
+             OffT* __restrict__ cursor, const OffT* __restrict__ part_start, uint32_t nb1,
+             const uint64_t* __restrict__ tile_prefix, uint64_t ntiles, uint64_t nparts,
+             typename EntryT<K, VT>::T* __restrict__ out) {
+    using ET = EntryT<K, VT>;
+    using E = typename ET::T;
+    using L = SplitLayout<K, VT, RAW>;
+    using InT = typename L::InT;
+    constexpr int kItems = L::kItems;
+    constexpr int kTile = L::kTile;
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char* const inb0 = smem;
+    unsigned char* const inb1 = smem + L::kInBytes;
+    E* const s_ent = reinterpret_cast<E*>(smem + 2 * L::kInBytes);
+    uint8_t* const s_dig = reinterpret_cast<uint8_t*>(s_ent + kTile);
+    __shared__ uint64_t s_bar[2];
+    __shared__ uint64_t s_t0[2], s_t1[2], s_cb[2];
+    __shared__ uint32_t s_ofs[2], s_ok[2];
+    __shared__ uint32_t s_cnt[kMaxDigits];
+    __shared__ uint32_t s_off[kMaxDigits];
+    __shared__ OffT s_gb[kMaxDigits];
+    __shared__ uint32_t s_wsum[kSplitBlock / 32];
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t ndig = dmask + 1;
+
+    // (thread 0) range of a tile; false when past the last real tile
+    auto tile_range = [&](uint64_t tile, uint64_t& t0, uint64_t& t1, uint64_t& cbase) -> bool {
+        if constexpr (PASS2) {
+            if (tile >= tile_prefix[nb1]) return false;
+            uint32_t lo = 0, hi = nb1;
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (tile_prefix[mid] <= tile) lo = mid; else hi = mid;
+            }
+            const uint64_t pe = (uint64_t(lo + 1) << b2) < nparts ? (uint64_t(lo + 1) << b2) : nparts;
+            const uint64_t bs = part_start[uint64_t(lo) << b2];
+            const uint64_t be = part_start[pe];
+            t0 = bs + (tile - tile_prefix[lo]) * kTile;
+            t1 = be < t0 + kTile ? be : t0 + kTile;
+            cbase = uint64_t(lo) << b2;
+        } else {
+            if (tile >= ntiles) return false;
+            t0 = tile * kTile;
+            t1 = n < t0 + kTile ? n : t0 + kTile;
+            cbase = 0;
+        }
+        return true;
+    };
+    auto issue = [&](uint64_t tile, int buf) {
+        uint64_t t0 = 0, t1 = 0, cb = 0;
+        const bool ok = tile_range(tile, t0, t1, cb);
+        s_ok[buf] = ok;
+        s_t0[buf] = t0;
+        s_t1[buf] = t1;
+        s_cb[buf] = cb;
+        if (ok) {
+            fence_proxy_async();
+            s_ofs[buf] = tma_load_span(buf ? inb1 : inb0, static_cast<const InT*>(in) + t0,
+                                       uint32_t((t1 - t0) * sizeof(InT)), &s_bar[buf]);
+        }
+    };
+
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        fence_mbar_init();
+        issue(blockIdx.x, 0);
+    }
+    __syncthreads();
+    uint64_t tile = blockIdx.x;
+    for (uint32_t it = 0;; ++it, tile += gridDim.x) {
+        const int buf = it & 1;
+        if (!s_ok[buf]) break;
+        if (tid == 0) issue(tile + gridDim.x, buf ^ 1);
+        const uint64_t t0 = s_t0[buf];
+        const uint32_t cnt = uint32_t(s_t1[buf] - t0);
+        const uint64_t cbase = s_cb[buf];
+        for (uint32_t d = tid; d < ndig; d += kSplitBlock) s_cnt[d] = 0;
+        mbar_wait(&s_bar[buf], (it >> 1) & 1);
+        const InT* src = reinterpret_cast<const InT*>((buf ? inb1 : inb0) + s_ofs[buf]);
+        __syncthreads();
+
+        uint32_t dr[kItems];  // digit << 16 | rank
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+            const uint32_t j = tid + k * kSplitBlock;
+            if (j < cnt) {
+                K key;
+                if constexpr (RAW) key = src[j]; else key = ET::key(src[j]);
+                const uint32_t p = uint32_t(hv<POW2>(key, seed, hk, nv) >> pshift);
+                const uint32_t d = (p >> dshift) & dmask;
+                dr[k] = (d << 16) | atomicAdd(s_cnt + d, 1u);
+            }
+        }
+        __syncthreads();
+        // exclusive scan of the <= 256 digit counts + run reservation
+        const uint32_t c = tid < ndig ? s_cnt[tid] : 0;
+        uint32_t inc = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+            if (int(lane) >= d) inc += y;
+        }
+        if (lane == 31) s_wsum[warp] = inc;
+        __syncthreads();
+        if (tid < ndig) {
+            uint32_t base = 0;
+            for (uint32_t w = 0; w < warp; ++w) base += s_wsum[w];
+            s_off[tid] = base + inc - c;
+            if (c) s_gb[tid] = atom_add(cursor + cbase + tid, OffT(c));
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+            const uint32_t j = tid + k * kSplitBlock;
+            if (j < cnt) {
+                const uint32_t d = dr[k] >> 16;
+                const uint32_t slot = s_off[d] + (dr[k] & 0xFFFFu);
+                if constexpr (RAW) {
+                    const K key = src[j];
+                    if constexpr (ET::kHasVal) {
+                        s_ent[slot] = ET::make(key, vals ? VT(vals[t0 + j]) : VT(t0 + j));
+                    } else {
+                        s_ent[slot] = ET::make(key, 0);
+                    }
+                } else {
+                    s_ent[slot] = src[j];
+                }
+                s_dig[slot] = uint8_t(d);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+            const uint32_t j = tid + k * kSplitBlock;
+            if (j < cnt) {
+                const uint32_t d = s_dig[j];
+                out[uint64_t(s_gb[d]) + (j - s_off[d])] = s_ent[j];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Pass-2 tile layout: tile_prefix[b] = sum over buckets < b of ceil(size/tile).
+template <typename OffT>
+__global__ void k_tile_prefix(const OffT* __restrict__ part_start, uint64_t nparts, uint32_t nb1,
+                              uint32_t b2, uint32_t kSplitTile, uint64_t* __restrict__ tile_prefix) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    uint64_t acc = 0;
+    for (uint32_t b = 0; b < nb1; ++b) {
+        tile_prefix[b] = acc;
+        const uint64_t hi = (uint64_t(b + 1) << b2) < nparts ? (uint64_t(b + 1) << b2) : nparts;
+        const uint64_t sz = uint64_t(part_start[hi]) - uint64_t(part_start[uint64_t(b) << b2]);
+        acc += (sz + kSplitTile - 1) / kSplitTile;
+    }
+    tile_prefix[nb1] = acc;
+}
+
+template <typename OffT>
+__global__ void k_init_cursors(const OffT* __restrict__ part_start, uint64_t nparts, uint32_t b2,
+                               uint32_t nb1, OffT* __restrict__ cur1, OffT* __restrict__ cur2) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < nparts; p += stride) {
+        cur2[p] = part_start[p];
+        if ((p & ((uint64_t(1) << b2) - 1)) == 0 && (p >> b2) < nb1) cur1[p >> b2] = part_start[p];
+    }
+}
+
+// Scratch for partition(): histogram, cursors, tile prefix, scan status and
+// one intermediate entry array (pass-1 output).
+template <typename K, typename VT, typename OffT>
+struct PartitionScratch {
+    using E = typename EntryT<K, VT>::T;
+    static size_t up(size_t x) { return (x + 255) / 256 * 256; }
+    static size_t bytes(const PartGeom& g, uint64_t n) {
+        return up((g.nparts + 1) * sizeof(OffT)) * 2 + up(((uint64_t(1) << g.b1) + 1) * sizeof(OffT)) +
+               up(((uint64_t(1) << g.b1) + 2) * 8) + up(scan_scratch_bytes(g.nparts)) +
+               (g.b2 ? up(n * sizeof(E)) : 0);
+    }
+};
+
+// Reorders n entries (raw keys [+ vals] on input) into partition order:
+// out[part_start[p] .. part_start[p+1]) holds the entries of partition p
+// (p = h(key) >> pshift). part_start (nparts + 1 entries, device) receives
+// the partition offsets; part_start[nparts] = n.
+template <typename K, typename VT, typename OffT, bool POW2>
+cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, int hk,
+                      const Divisor& nv, const PartGeom& g, OffT* part_start, void* scratch,
+                      typename EntryT<K, VT>::T* out, cudaStream_t s, const char* tag) {
+    using PS = PartitionScratch<K, VT, OffT>;
+    using E = typename EntryT<K, VT>::T;
+    char* p = static_cast<char*>(scratch);
+    OffT* hist = reinterpret_cast<OffT*>(p);
+    p += PS::up((g.nparts + 1) * sizeof(OffT));
+    OffT* cur2 = reinterpret_cast<OffT*>(p);
+    p += PS::up((g.nparts + 1) * sizeof(OffT));
+    OffT* cur1 = reinterpret_cast<OffT*>(p);
+    p += PS::up(((uint64_t(1) << g.b1) + 1) * sizeof(OffT));
+    uint64_t* tile_prefix = reinterpret_cast<uint64_t*>(p);
+    p += PS::up(((uint64_t(1) << g.b1) + 2) * 8);
+    void* scan_scr = p;
+    p += PS::up(scan_scratch_bytes(g.nparts));
+    E* mid = reinterpret_cast<E*>(p);
+
+    cudaError_t e = cudaMemsetAsync(hist, 0, g.nparts * sizeof(OffT), s);
+    if (e != cudaSuccess) return e;
+    const int sms = num_sms();
+    const size_t hsmem = ((g.nparts + 1) / 2) * 4;
+    auto kh = k_part_hist<K, OffT, POW2>;
+    if (hsmem > 48 * 1024 &&
+        (e = cudaFuncSetAttribute(kh, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hsmem))) !=
+            cudaSuccess)
+        return e;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kh, kHistBlock, hsmem);
+    unsigned grid = unsigned(std::max(1, per_sm) * sms);
+    grid = unsigned(std::max<uint64_t>(
+        1, std::min<uint64_t>(grid, (n + kHistBlock * 16 - 1) / (kHistBlock * 16))));
+    HG_LAUNCH(tag, s, kh<<<grid, kHistBlock, hsmem, s>>>(keys, n, seed, hk, nv, g.pshift,
+                                                        uint32_t(g.nparts), hist));
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = launch_scan<OffT, OffT>(hist, part_start, g.nparts, scan_scr, part_start + g.nparts, s,
+                                     "part_scan")) != cudaSuccess)
+        return e;
+    const uint32_t nb1 = uint32_t((g.nparts + (uint64_t(1) << g.b2) - 1) >> g.b2);
+    k_init_cursors<OffT><<<unsigned(std::min<uint64_t>((g.nparts + 255) / 256, 1024)), 256, 0, s>>>(
+        part_start, g.nparts, g.b2, nb1, cur1, cur2);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    constexpr int kSplitTile = split_tile<E>();
+    const uint64_t tiles1 = (n + kSplitTile - 1) / kSplitTile;
+    auto ks1 = k_multisplit<K, VT, OffT, true, false, POW2>;
+    auto ks2 = k_multisplit<K, VT, OffT, false, true, POW2>;
+    constexpr size_t sm1 = SplitLayout<K, VT, true>::kBytes;
+    constexpr size_t sm2 = SplitLayout<K, VT, false>::kBytes;
+    if ((e = cudaFuncSetAttribute(ks1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm1))) !=
+            cudaSuccess ||
+        (e = cudaFuncSetAttribute(ks2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm2))) !=
+            cudaSuccess)
+        return e;
+    int occ1 = 0, occ2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, ks1, kSplitBlock, sm1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, ks2, kSplitBlock, sm2);
+    const unsigned g1 = unsigned(std::max<uint64_t>(
+        1, std::min<uint64_t>(tiles1, uint64_t(sms) * std::max(1, occ1))));
+    const unsigned g2 = unsigned(std::max<uint64_t>(
+        1, std::min<uint64_t>(tiles1 + 1, uint64_t(sms) * std::max(1, occ2))));
+    if (g.b2 == 0) {
+        // single pass straight into partition order
+        HG_LAUNCH("multisplit1", s,
+                  (ks1<<<g1, kSplitBlock, sm1, s>>>(
+                      keys, vals, n, seed, hk, nv, g.pshift, 0, uint32_t((1u << g.b1) - 1), 0,
+                      cur2, part_start, 0, nullptr, tiles1, g.nparts, out)));
+        return cudaGetLastError();
+    }
+    HG_LAUNCH("multisplit1", s,
+              (ks1<<<g1, kSplitBlock, sm1, s>>>(
+                  keys, vals, n, seed, hk, nv, g.pshift, g.b2, uint32_t((1u << g.b1) - 1), 0, cur1,
+                  part_start, 0, nullptr, tiles1, g.nparts, mid)));
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    k_tile_prefix<OffT><<<1, 32, 0, s>>>(part_start, g.nparts, nb1, g.b2, kSplitTile, tile_prefix);
+    const uint64_t tiles2 = tiles1 + nb1;  // upper bound; exact count = tile_prefix[nb1]
+    HG_LAUNCH("multisplit2", s,
+              (ks2<<<g2, kSplitBlock, sm2, s>>>(
+                  mid, nullptr, n, seed, hk, nv, g.pshift, 0, uint32_t((1u << g.b2) - 1), g.b2,
+                  cur2, part_start, nb1, tile_prefix, tiles2, g.nparts, out)));
+    return cudaGetLastError();
+}
+
+}  // namespace hg

@@ -357,9 +357,10 @@ def build_v2(keys, cfg: Optional[BuildConfig] = None, stats: Optional[BuildStats
 
 
 def probe_standard(hg: HashGraph, probe_keys, opts: Optional[ProbeOptions] = None,
-                   counts=None) -> JoinResult:
+                   counts=None, method: int = 0) -> JoinResult:
     """join.hpp:110-136. `counts` (optional, length-m uint32 array / CUDA
-    tensor) receives each probe's match count."""
+    tensor) receives each probe's match count. method: 0 auto, 1 direct
+    gathers, 2 vertex-range partitioned probes."""
     opts = opts or ProbeOptions()
     pa = _Arr(probe_keys, np.uint64 if hg.key_width == 8 else np.uint32)
     if pa.width == 8 and hg.key_width == 4:
@@ -373,6 +374,7 @@ def probe_standard(hg: HashGraph, probe_keys, opts: Optional[ProbeOptions] = Non
     o.materialize = 1 if opts.materialize else 0
     o.pair_width = 8
     o.pair_cap = int(opts.pair_cap)
+    o.method = int(method)
     pairs = None
     if opts.materialize:
         pairs = np.zeros(max(min(int(opts.pair_cap), max(pa.n, 1) * max(hg.num_edges(), 1)), 0),
@@ -394,7 +396,7 @@ def probe_standard(hg: HashGraph, probe_keys, opts: Optional[ProbeOptions] = Non
 
 
 def probe_device(hg: HashGraph, probes, device_result, counts=None, pairs=None,
-                 pair_width: int = 4, pair_cap: int = 0, stream=None) -> None:
+                 pair_width: int = 4, pair_cap: int = 0, stream=None, method: int = 0) -> None:
     """Fully asynchronous probe_standard on device-resident data: totals
     {match_count, key_comparisons} land in `device_result` (CUDA u64[2]
     tensor); optional per-probe `counts` (u32) and `pairs` (pair_width 4:
@@ -403,6 +405,7 @@ def probe_device(hg: HashGraph, probes, device_result, counts=None, pairs=None,
     o = _lib.hg_probe_options()
     _lib.lib().hg_probe_options_init(C.byref(o))
     o.device_result = ra.ptr
+    o.method = int(method)
     if counts is not None:
         o.counts = _Arr(counts).ptr
     if pairs is not None:

@@ -204,21 +204,28 @@ def test_random_vs_oracle(oracle, n, kr, load, seed, width, variant, agg, bins):
                                                       dtype=np.uint64)])
     if width == 4:
         probes &= np.uint64(0xFFFFFFFF)
-    r = hg.probe_standard(t, probes.astype(dt), ProbeOptions(materialize=True, pair_cap=1 << 26))
-    ro = oracle.probe_standard(o, probes, materialize=True, cap=1 << 26)
-    assert r.match_count == ro["match_count"]
-    assert r.key_comparisons == ro["key_comparisons"]
-    assert not r.truncated
-    got = np.stack([r.pairs["left_index"], r.pairs["right_index"]], 1)
-    exp = ro["pairs"]
-    got = got[np.lexsort((got[:, 0], got[:, 1]))]
-    exp = exp[np.lexsort((exp[:, 0], exp[:, 1]))]
-    assert (got == exp).all()
-    # per-probe counts == count_instances per key
-    counts = np.zeros(len(probes), np.uint32)
-    hg.probe_standard(t, probes.astype(dt), counts=counts)
-    ro2 = oracle.probe_standard(o, probes, per_probe=True)
-    assert (counts.astype(np.uint64) == ro2["per_probe"]).all()
+    ro = oracle.probe_standard(o, probes, materialize=True, cap=1 << 26, per_probe=True)
+    exp = ro["pairs"][np.lexsort((ro["pairs"][:, 0], ro["pairs"][:, 1]))]
+    for method in (1, 2):  # direct gathers, vertex-range partitioned
+        r = hg.probe_standard(t, probes.astype(dt), ProbeOptions(materialize=True, pair_cap=1 << 26),
+                              method=method)
+        assert r.match_count == ro["match_count"]
+        assert r.key_comparisons == ro["key_comparisons"]
+        assert not r.truncated
+        got = np.stack([r.pairs["left_index"], r.pairs["right_index"]], 1)
+        got = got[np.lexsort((got[:, 0], got[:, 1]))]
+        assert (got == exp).all()
+        # per-probe counts == count_instances per key (count-only and with pairs)
+        counts = np.zeros(len(probes), np.uint32)
+        r2 = hg.probe_standard(t, probes.astype(dt), counts=counts, method=method)
+        assert r2.match_count == ro["match_count"] and r2.key_comparisons == ro["key_comparisons"]
+        assert (counts.astype(np.uint64) == ro["per_probe"]).all()
+        counts[:] = 0
+        hg.probe_standard(t, probes.astype(dt), ProbeOptions(materialize=True, pair_cap=1 << 26),
+                          counts=counts, method=method)
+        assert (counts.astype(np.uint64) == ro["per_probe"]).all()
+        r3 = hg.probe_standard(t, probes.astype(dt), method=method)
+        assert (r3.match_count, r3.key_comparisons) == (ro["match_count"], ro["key_comparisons"])
 
 
 def test_probe_cap_truncation():
@@ -266,13 +273,15 @@ def test_long_segments_warp_cooperative(oracle):
         t = BUILDS[variant](keys, BuildConfig(mode=ExecMode.sequential))
         assert_same_table(t, o, exact=True)
     probes = np.array([11, 12, 13] * 50 + [11] * 3, np.uint64)
-    r = hg.probe_standard(t, probes, ProbeOptions(materialize=True, pair_cap=1 << 24))
     ro = oracle.probe_standard(o, probes, materialize=True, cap=1 << 24)
-    assert r.match_count == ro["match_count"] and r.key_comparisons == ro["key_comparisons"]
-    got = np.stack([r.pairs["left_index"], r.pairs["right_index"]], 1)
-    got = got[np.lexsort((got[:, 0], got[:, 1]))]
     exp = ro["pairs"][np.lexsort((ro["pairs"][:, 0], ro["pairs"][:, 1]))]
-    assert (got == exp).all()
+    for method in (1, 2):
+        r = hg.probe_standard(t, probes, ProbeOptions(materialize=True, pair_cap=1 << 24),
+                              method=method)
+        assert r.match_count == ro["match_count"] and r.key_comparisons == ro["key_comparisons"]
+        got = np.stack([r.pairs["left_index"], r.pairs["right_index"]], 1)
+        got = got[np.lexsort((got[:, 0], got[:, 1]))]
+        assert (got == exp).all()
 
 
 def test_device_tensors_in_place(oracle, cuda):
@@ -290,3 +299,32 @@ def test_device_tensors_in_place(oracle, cuda):
     ro = oracle.probe_standard(o, host, per_probe=True)
     assert r.match_count == ro["match_count"]
     assert (counts.cpu().numpy().view(np.uint32).astype(np.uint64) == ro["per_probe"]).all()
+
+
+@pytest.mark.parametrize("log2n,width,load", [(22, 4, 1.0), (24, 4, 1.0), (23, 8, 0.5),
+                                              (23, 4, 4.0), (22, 8, 1.5)])
+def test_large_scale_vs_oracle(oracle, cuda, log2n, width, load):
+    """Sizes where the partitioned (multi-pass) paths are the ones that run."""
+    torch = cuda
+    n = 1 << log2n
+    dt = torch.int32 if width == 4 else torch.int64
+    keys = torch.empty(n, dtype=dt, device="cuda")
+    probes = torch.empty(n, dtype=dt, device="cuda")
+    hg.generate(keys, kind=0, seed=11)
+    hg.generate(probes, kind=0, seed=12)
+    hk = keys.cpu().numpy().view(np.uint32 if width == 4 else np.uint64).astype(np.uint64)
+    hp = probes.cpu().numpy().view(np.uint32 if width == 4 else np.uint64).astype(np.uint64)
+    o = oracle.build(hk, 1, load)
+    for variant in (1, 2):
+        t = BUILDS[variant](keys, BuildConfig(load_factor=load))
+        assert_same_table(t, o, exact=False)
+        assert hg.validate_csr(t, n, keys) is None
+    half = np.concatenate([hk[: n // 2], hp[: n // 2]])
+    ro = oracle.probe_standard(o, half)
+    dhalf = torch.cat([keys[: n // 2], probes[: n // 2]])
+    for method in (1, 2):
+        r = hg.probe_standard(t, dhalf, method=method)
+        assert (r.match_count, r.key_comparisons) == (ro["match_count"], ro["key_comparisons"])
+    res = torch.zeros(2, dtype=torch.int64, device="cuda")
+    hg.probe_device(t, dhalf, res, method=2)
+    assert [int(x) for x in res.cpu()] == [ro["match_count"], ro["key_comparisons"]]
