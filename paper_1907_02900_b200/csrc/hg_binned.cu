@@ -27,99 +27,143 @@ namespace hg {
 
 // ---------------------------------------------------------------- K7
 
-// K7 shared-memory layout (1 CTA of 1024 threads per SM):
-//   cnt[P] u32 | lv[cap] u16 | in[2][cap] entries (TMA double buffer) | keys[cap] | vals[cap]
+// K7: partitions are assigned round-robin to CTAs (two CTAs per SM). Per
+// partition:
+//   * its entries arrive by one TMA bulk copy, issued while the previous
+//     partition is still being processed (the partition bounds are loaded two
+//     partitions ahead), and are moved into registers (kItems per thread);
+//   * each entry's rank within its vertex is the old value returned by its
+//     shared-memory count atomic, so placement needs no second atomic;
+//   * keys / values are placed into shared-memory staging arrays and written
+//     back with TMA bulk stores (cp.async.bulk global<-shared) that overlap
+//     the next partition; offsets go out as 16-byte vector stores.
+// Shared memory: cnt[P] u32 | in[cap] entries | keys[cap+4] | vals[cap+4].
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+constexpr int kBuildBlock = 512;
 
 template <typename K, typename VT>
 struct BuildLayout {
     using E = typename EntryT<K, VT>::T;
-    __host__ __device__ static size_t in_bytes(uint32_t cap) { return align16(size_t(cap) * sizeof(E) + 32); }
-    static size_t bytes(uint32_t P, uint32_t cap) {
-        return align16(size_t(P) * 4) + align16(size_t(cap) * 2) + 2 * in_bytes(cap) +
-               align16(size_t(cap) * sizeof(K)) + align16(size_t(cap) * sizeof(VT));
-    }
-    static uint32_t cap_for(uint32_t P, size_t budget) {
-        const size_t fixed = align16(size_t(P) * 4) + 5 * 16 + 64;
-        if (budget <= fixed) return 0;
-        return uint32_t((budget - fixed) / (2 + 2 * sizeof(E) + sizeof(K) + sizeof(VT))) & ~7u;
-    }
+    static constexpr int kItems = sizeof(E) >= 16 ? 6 : 10;
+    static constexpr uint32_t kCap = kBuildBlock * kItems;  // staged entries per partition
+    __host__ __device__ static size_t in_bytes() { return align16(size_t(kCap) * sizeof(E) + 32); }
+    __host__ __device__ static size_t k_bytes() { return align16(size_t(kCap + 4) * sizeof(K)); }
+    __host__ __device__ static size_t v_bytes() { return align16(size_t(kCap + 4) * sizeof(VT)); }
+    static size_t bytes(uint32_t P) { return align16(size_t(P) * 4) + in_bytes() + k_bytes() + v_bytes(); }
 };
 
-constexpr int kBuildBlock = 1024;
-
 template <typename K, typename VT, typename OffT, bool POW2>
-__global__ void __launch_bounds__(kBuildBlock, 1)
+__global__ void __launch_bounds__(kBuildBlock)
 k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
              const OffT* __restrict__ part_start /* nparts + 1 partition offsets */,
              uint64_t nparts, uint64_t nv_total, uint64_t seed, int hk, Divisor nv,
-             uint32_t pshift, uint32_t cap, OffT* __restrict__ offs, K* __restrict__ okeys,
+             uint32_t pshift, OffT* __restrict__ offs, K* __restrict__ okeys,
              VT* __restrict__ ovals) {
     using PE = EntryT<K, VT>;
     using E = typename PE::T;
     using L = BuildLayout<K, VT>;
+    constexpr int kItems = L::kItems;
+    constexpr uint32_t cap = L::kCap;
+    constexpr uint32_t KA = 16 / sizeof(K), VA = 16 / sizeof(VT);
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t P = 1u << pshift;
     uint32_t* cnt = reinterpret_cast<uint32_t*>(smem);
-    uint16_t* lvs = reinterpret_cast<uint16_t*>(smem + align16(size_t(P) * 4));
-    unsigned char* inb0 = reinterpret_cast<unsigned char*>(lvs) + align16(size_t(cap) * 2);
-    unsigned char* inb1 = inb0 + L::in_bytes(cap);
-    K* sk = reinterpret_cast<K*>(inb1 + L::in_bytes(cap));
-    VT* sv = reinterpret_cast<VT*>(reinterpret_cast<unsigned char*>(sk) + align16(size_t(cap) * sizeof(K)));
-    __shared__ uint64_t s_bar[2];
-    __shared__ uint64_t s_s[2], s_e[2];
-    __shared__ uint32_t s_ofs[2];
+    unsigned char* inb = smem + align16(size_t(P) * 4);
+    K* sk = reinterpret_cast<K*>(inb + L::in_bytes());
+    VT* sv = reinterpret_cast<VT*>(reinterpret_cast<unsigned char*>(sk) + L::k_bytes());
+    __shared__ uint64_t s_bar;
+    __shared__ uint64_t s_s, s_e;
+    __shared__ uint32_t s_ofs;
     __shared__ uint32_t s_warp[kBuildBlock / 32];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr uint32_t nwarps = kBuildBlock / 32;
+    const uint64_t step = gridDim.x;
 
-    auto issue = [&](uint64_t p, int buf) {  // thread 0
-        if (p >= nparts) return;
-        const uint64_t s = part_start[p], e = part_start[p + 1];
-        s_s[buf] = s;
-        s_e[buf] = e;
+    // thread 0: bounds of the partition after the next one (prefetched)
+    uint64_t n_s = 0, n_e = 0;
+    auto issue = [&](uint64_t s, uint64_t e) {  // thread 0
         if (e - s <= cap) {
             fence_proxy_async();
-            s_ofs[buf] = tma_load_span(buf ? inb1 : inb0, reorg + s, uint32_t((e - s) * sizeof(E)),
-                                       &s_bar[buf]);
+            s_ofs = tma_load_span(inb, reorg + s, uint32_t((e - s) * sizeof(E)), &s_bar);
         }
     };
     if (tid == 0) {
-        mbar_init(&s_bar[0], 1);
-        mbar_init(&s_bar[1], 1);
+        mbar_init(&s_bar, 1);
         fence_mbar_init();
-        issue(blockIdx.x, 0);
+        const uint64_t p0 = blockIdx.x;
+        if (p0 < nparts) {
+            s_s = part_start[p0];
+            s_e = part_start[p0 + 1];
+            issue(s_s, s_e);
+        }
+        if (p0 + step < nparts) {
+            n_s = part_start[p0 + step];
+            n_e = part_start[p0 + step + 1];
+        }
     }
     __syncthreads();
-    uint32_t use[2] = {0, 0};
-    for (uint64_t p = blockIdx.x, it = 0; p < nparts; p += gridDim.x, ++it) {
-        const int buf = int(it & 1);
-        const uint64_t s = s_s[buf], e = s_e[buf];
+    uint32_t phase = 0;
+    for (uint64_t p = blockIdx.x; p < nparts; p += step) {
+        const uint64_t s = s_s, e = s_e;
         const uint32_t cntp = uint32_t(e - s);
-        const bool staged = uint64_t(cntp) <= cap;
-        if (tid == 0) issue(p + gridDim.x, buf ^ 1);
+        const bool staged = cntp <= cap;
         const uint64_t vb = p << pshift;
         const uint32_t pv = uint32_t(nv_total - vb < P ? nv_total - vb : uint64_t(P));
         for (uint32_t j = tid; j < pv; j += kBuildBlock) cnt[j] = 0;
+        E ent[kItems];
         if (staged) {
-            mbar_wait(&s_bar[buf], use[buf] & 1);
-            ++use[buf];
+            mbar_wait(&s_bar, phase);
+            phase ^= 1;
+            const E* src = reinterpret_cast<const E*>(inb + s_ofs);
+#pragma unroll
+            for (int k = 0; k < kItems; ++k) {
+                const uint32_t i = tid + k * kBuildBlock;
+                if (i < cntp) ent[k] = src[i];
+            }
         }
-        const E* src = staged ? reinterpret_cast<const E*>((buf ? inb1 : inb0) + s_ofs[buf])
-                              : reorg + s;
-        __syncthreads();
-        // count: the second hash evaluation of V2's create_table pass (core.hpp:126-133)
-        for (uint32_t i = tid; i < cntp; i += kBuildBlock) {
-            const uint32_t lv = uint32_t(hv<POW2>(PE::key(src[i]), seed, hk, nv) - vb);
-            if (staged) lvs[i] = uint16_t(lv);
-            atomicAdd(cnt + lv, 1u);
+        __syncthreads();  // cnt zeroed, input buffer consumed
+        if (tid == 0) {
+            // next partition's entries stream in while this one is built
+            const uint64_t pn = p + step;
+            if (pn < nparts) issue(n_s, n_e);
+            s_s = n_s;
+            s_e = n_e;
+            if (pn + step < nparts) {
+                n_s = part_start[pn + step];
+                n_e = part_start[pn + step + 1];
+            }
+        }
+        // count: the second hash evaluation of V2's create_table pass
+        // (core.hpp:126-133); the returned count is the entry's rank
+        uint32_t lr[kItems];
+        if (staged) {
+#pragma unroll
+            for (int k = 0; k < kItems; ++k) {
+                const uint32_t i = tid + k * kBuildBlock;
+                if (i < cntp) {
+                    const uint32_t lv = uint32_t(hv<POW2>(PE::key(ent[k]), seed, hk, nv) - vb);
+                    lr[k] = (lv << 16) | atomicAdd(cnt + lv, 1u);
+                }
+            }
+        } else {
+            for (uint32_t i = tid; i < cntp; i += kBuildBlock) {
+                const uint32_t lv = uint32_t(hv<POW2>(PE::key(reorg[s + i]), seed, hk, nv) - vb);
+                atomicAdd(cnt + lv, 1u);
+            }
         }
         __syncthreads();
-        // exclusive scan of cnt[0..pv): each thread owns a contiguous run
+        // exclusive scan of cnt[0..pv): thread owns `per` consecutive counters
         const uint32_t per = (pv + kBuildBlock - 1) / kBuildBlock;
         const uint32_t j0 = min(pv, tid * per), j1 = min(pv, j0 + per);
         uint32_t run = 0;
-        for (uint32_t j = j0; j < j1; ++j) run += cnt[j];
+        const bool vec4 = per == 4 && j1 - j0 == 4;
+        uint4 c4 = make_uint4(0, 0, 0, 0);
+        if (vec4) {
+            c4 = *reinterpret_cast<const uint4*>(cnt + j0);
+            run = c4.x + c4.y + c4.z + c4.w;
+        } else {
+            for (uint32_t j = j0; j < j1; ++j) run += cnt[j];
+        }
         uint32_t inc = run;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -129,49 +173,72 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
         if (lane == 31) s_warp[warp] = inc;
         __syncthreads();
         if (warp == 0) {
-            const uint32_t w = s_warp[lane];
+            const uint32_t w = lane < kBuildBlock / 32 ? s_warp[lane] : 0;
             uint32_t wi = w;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, wi, d);
                 if (int(lane) >= d) wi += y;
             }
-            s_warp[lane] = wi - w;
+            if (lane < kBuildBlock / 32) s_warp[lane] = wi - w;
         }
         __syncthreads();
         uint32_t acc = s_warp[warp] + inc - run;
-        for (uint32_t j = j0; j < j1; ++j) {
-            const uint32_t c = cnt[j];
-            cnt[j] = acc;  // exclusive start = placement cursor
-            acc += c;
-            offs[vb + j + 1] = OffT(s + acc);  // end(j) (contiguous per thread)
-        }
-        if (p == 0 && tid == 0) offs[0] = 0;
-        __syncthreads();
-        if (staged) {
-            for (uint32_t i = tid; i < cntp; i += kBuildBlock) {
-                const E ent = src[i];
-                const uint32_t pos = atomicAdd(cnt + lvs[i], 1u);
-                sk[pos] = PE::key(ent);
-                sv[pos] = PE::val(ent);
-            }
-            __syncthreads();
-            for (uint32_t i = tid; i < cntp; i += kBuildBlock) {
-                okeys[s + i] = sk[i];
-                ovals[s + i] = sv[i];
+        if (vec4) {
+            const uint4 st = make_uint4(acc, acc + c4.x, acc + c4.x + c4.y, acc + c4.x + c4.y + c4.z);
+            *reinterpret_cast<uint4*>(cnt + j0) = st;
+            if constexpr (sizeof(OffT) == 4) {
+                // offs + 1 is 16-byte aligned (hg_capi pads it) and vb + j0 is a multiple of 4
+                *reinterpret_cast<uint4*>(offs + vb + j0 + 1) =
+                    make_uint4(uint32_t(s) + st.y, uint32_t(s) + st.z, uint32_t(s) + st.w,
+                               uint32_t(s) + acc + run);
+            } else {
+                offs[vb + j0 + 1] = OffT(s + st.y);
+                offs[vb + j0 + 2] = OffT(s + st.z);
+                offs[vb + j0 + 3] = OffT(s + st.w);
+                offs[vb + j0 + 4] = OffT(s + acc + run);
             }
         } else {
+            for (uint32_t j = j0; j < j1; ++j) {
+                const uint32_t c = cnt[j];
+                cnt[j] = acc;  // exclusive start
+                acc += c;
+                offs[vb + j + 1] = OffT(s + acc);  // end(j)
+            }
+        }
+        if (p == 0 && tid == 0) offs[0] = 0;
+        // the previous partition's bulk stores must have read the staging arrays
+        if (tid == 0) bulk_wait_read();
+        __syncthreads();
+        if (staged) {
+            K* skp = sk + (s & (KA - 1));
+            VT* svp = sv + (s & (VA - 1));
+#pragma unroll
+            for (int k = 0; k < kItems; ++k) {
+                const uint32_t i = tid + k * kBuildBlock;
+                if (i < cntp) {
+                    const uint32_t pos = cnt[lr[k] >> 16] + (lr[k] & 0xFFFFu);
+                    skp[pos] = PE::key(ent[k]);
+                    svp[pos] = PE::val(ent[k]);
+                }
+            }
+            fence_proxy_async();
+            __syncthreads();
+            const bool a = bulk_store_span(okeys + s, skp, cntp, tid, kBuildBlock);
+            const bool b = bulk_store_span(ovals + s, svp, cntp, tid, kBuildBlock);
+            if (a || b) bulk_commit();
+        } else {
             for (uint32_t i = tid; i < cntp; i += kBuildBlock) {
-                const E ent = src[i];
-                const uint32_t lv = uint32_t(hv<POW2>(PE::key(ent), seed, hk, nv) - vb);
+                const E en = reorg[s + i];
+                const uint32_t lv = uint32_t(hv<POW2>(PE::key(en), seed, hk, nv) - vb);
                 const uint64_t pos = s + atomicAdd(cnt + lv, 1u);
-                okeys[pos] = PE::key(ent);
-                ovals[pos] = PE::val(ent);
+                okeys[pos] = PE::key(en);
+                ovals[pos] = PE::val(en);
             }
         }
         __syncthreads();
     }
-    (void)nwarps;
+    if (tid == 0) bulk_wait_all();
 }
 
 template <typename K, typename VT, typename OffT, bool POW2>
@@ -186,12 +253,11 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
     cudaGetDevice(&dev);
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    const size_t budget = size_t(smem_optin) - 2048;
-    // ~4096 entries per partition; K7 stages up to `cap` entries per partition
-    const PartGeom g = make_geom(t.nv, t.n, a.partition_vertices, 4096.0);
-    const uint32_t cap = std::min<uint32_t>(BuildLayout<K, VT>::cap_for(1u << g.pshift, budget),
-                                            65535u);
-    const size_t smem = BuildLayout<K, VT>::bytes(1u << g.pshift, cap);
+    (void)smem_optin;
+    // ~4096 entries per partition (2048 for 16-byte entries); K7 stages up
+    // to BuildLayout::kCap entries of a partition in shared memory
+    const PartGeom g = make_geom(t.nv, t.n, a.partition_vertices, sizeof(E) >= 16 ? 2048.0 : 4096.0);
+    const size_t smem = BuildLayout<K, VT>::bytes(1u << g.pshift);
 
     const size_t ps_bytes = ((g.nparts + 1) * sizeof(OffT) + 255) & ~size_t(255);
     const size_t pscr = PartitionScratch<K, VT, OffT>::bytes(g, t.n);
@@ -203,7 +269,9 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
     OffT* part_start = reinterpret_cast<OffT*>(scratch);
     void* pscratch = scratch + ps_bytes;
     E* reorg = reinterpret_cast<E*>(scratch + ps_bytes + pscr);
+    uint32_t* ticket = reinterpret_cast<uint32_t*>(scratch + ps_bytes + pscr + reorg_bytes);
     do {
+        if ((e = cudaMemsetAsync(ticket, 0, 4, s)) != cudaSuccess) break;
         e = partition<K, VT, OffT, POW2>(static_cast<const K*>(a.keys),
                                          static_cast<const VT*>(a.vals), t.n, t.seed, t.hash_kind,
                                          nv, g, part_start, pscratch, reorg, s, "k4_part_hist");
@@ -218,7 +286,7 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
             std::min<uint64_t>(uint64_t(std::max(1, per_sm)) * num_sms(), g.nparts));
         HG_LAUNCH("k7_part_build", s,
                   kb<<<gk, kBuildBlock, smem, s>>>(reorg, part_start, g.nparts, t.nv, t.seed,
-                                                   t.hash_kind, nv, g.pshift, cap, offs,
+                                                   t.hash_kind, nv, g.pshift, offs,
                                                    static_cast<K*>(t.keys),
                                                    static_cast<VT*>(t.vals)));
         e = cudaGetLastError();

@@ -218,6 +218,10 @@ hg_status hg_build(const void* keys, int32_t key_width, const void* vals, int32_
         hg_status st = hg_derived_vertex_count(n, cfg.load_factor, &nv);
         if (st != HG_OK) return st;
     }
+    if (cfg.variant == HG_BUILD_BINNED && nv > (uint64_t(1) << 30))
+        return fail(HG_EUNSUPPORTED,
+                    "binned build supports up to 2^30 vertices per device (two 8-bit partition "
+                    "digits); shard the table by hash range or use the simple build");
     int dev = 0;
     if (hg_status st = need_device(&dev); st != HG_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);

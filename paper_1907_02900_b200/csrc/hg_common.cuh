@@ -157,6 +157,52 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// global <- shared bulk store (async proxy), bytes % 16 == 0, both 16-byte aligned.
+__device__ __forceinline__ void tma_store_1d(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_addr(src)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// Waits until all committed bulk stores of this thread have finished reading
+// shared memory (the staging buffer may be overwritten afterwards).
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// Waits until all committed bulk stores of this thread are complete.
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// Stores elements [0, n) of a shared staging array `src` to global `dst`
+// where src[0] corresponds to dst[0] and (dst - src) is a multiple of 16
+// bytes in address alignment terms (i.e. both have the same address & 15).
+// The 16-byte-aligned middle goes out as one bulk copy issued by `lane0`
+// (returns true when it issued one); the unaligned head and tail elements
+// are stored by the calling threads (tid/nthreads). Caller must have fenced
+// (fence_proxy_async) + synchronised the staging writes beforehand.
+template <typename T>
+__device__ __forceinline__ bool bulk_store_span(T* dst, const T* src, uint32_t n, uint32_t tid,
+                                                uint32_t nthreads) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(dst);
+    const uint32_t head = uint32_t(((16 - (a & 15)) & 15) / sizeof(T));
+    const uint32_t h = head < n ? head : n;
+    const uint32_t body = ((n - h) * sizeof(T)) & ~uint32_t(15);
+    const uint32_t body_n = body / sizeof(T);
+    for (uint32_t i = tid; i < h; i += nthreads) dst[i] = src[i];
+    for (uint32_t i = h + body_n + tid; i < n; i += nthreads) dst[i] = src[i];
+    if (tid == 0 && body) {
+        tma_store_1d(dst + h, src + h, body);
+        return true;
+    }
+    return false;
+}
+
 // Issues the 16-byte-aligned superset of global bytes [src, src + bytes) into
 // dst; returns the byte offset of src inside dst. Caller's buffer must hold
 // bytes + 32.

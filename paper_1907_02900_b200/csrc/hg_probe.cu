@@ -220,45 +220,97 @@ k_probe_write(const K* __restrict__ probes, uint64_t m, uint64_t seed, int hk, D
 
 constexpr int kPartProbeBlock = 512;
 
+// Shared memory per CTA: offsets slice (P+1) | table keys slice (kcap) |
+// probe entries of the partition (pcap), all filled by TMA bulk copies.
+template <typename K, typename OffT, typename PEnt>
+struct ProbeLayout {
+    __host__ __device__ static size_t off_bytes(uint32_t P) { return (size_t(P + 1) * sizeof(OffT) + 32 + 15) & ~size_t(15); }
+    __host__ __device__ static size_t key_bytes(uint32_t kcap) { return (size_t(kcap) * sizeof(K) + 32 + 15) & ~size_t(15); }
+    __host__ __device__ static size_t ent_bytes(uint32_t pcap) { return (size_t(pcap) * sizeof(PEnt) + 32 + 15) & ~size_t(15); }
+    static size_t bytes(uint32_t P, uint32_t kcap, uint32_t pcap) {
+        return off_bytes(P) + key_bytes(kcap) + ent_bytes(pcap);
+    }
+};
+
 // MODE 0: totals only; 1: totals + per-probe count at the probe's partitioned
 // position (pcount[pos]) or, with ORIG, at its original index; 2: pairs.
+// One partition per CTA iteration: thread 0 issues TMA bulk loads of the
+// partition's offsets slice, its table-key slice and its probe entries into
+// shared memory (one mbarrier), then every probe is answered from shared
+// memory. Slices larger than the caps are read from global memory instead.
 template <typename K, typename VT, typename OffT, typename IT, bool POW2, int MODE, bool ORIG,
           typename PT>
 __global__ void __launch_bounds__(kPartProbeBlock)
 k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __restrict__ ppart,
              uint64_t nparts, uint64_t nv_total, uint64_t seed, int hk, Divisor nv,
              uint32_t pshift, const OffT* __restrict__ offs, const K* __restrict__ tkeys,
-             const VT* __restrict__ tvals, uint32_t kcap, uint32_t* __restrict__ pcount,
-             const uint64_t* __restrict__ pair_off, void* __restrict__ pairs, uint64_t cap,
-             uint64_t* __restrict__ totals, uint32_t* ticket) {
+             const VT* __restrict__ tvals, uint32_t kcap, uint32_t pcap,
+             uint32_t* __restrict__ pcount, const uint64_t* __restrict__ pair_off,
+             void* __restrict__ pairs, uint64_t cap, uint64_t* __restrict__ totals,
+             uint32_t* ticket) {
     using PE = EntryT<K, IT>;
+    using PEnt = typename PE::T;
+    using L = ProbeLayout<K, OffT, PEnt>;
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t P = 1u << pshift;
-    uint32_t* soff = reinterpret_cast<uint32_t*>(smem);
-    K* skeys = reinterpret_cast<K*>(smem + ((size_t(P + 1) * 4 + 15) & ~size_t(15)));
-    __shared__ uint32_t s_part;
+    unsigned char* const b_off = smem;
+    unsigned char* const b_key = smem + L::off_bytes(P);
+    unsigned char* const b_ent = b_key + L::key_bytes(kcap);
+    __shared__ uint64_t s_bar;
+    __shared__ uint64_t s_p, s_tb, s_te, s_q0, s_q1;
+    __shared__ uint32_t s_o0, s_o1, s_o2, s_kst, s_pst;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t nwarps = kPartProbeBlock / 32;
+    constexpr uint32_t nwarps = kPartProbeBlock / 32;
+    if (tid == 0) {
+        mbar_init(&s_bar, 1);
+        fence_mbar_init();
+    }
+    uint32_t phase = 0;
     uint64_t matches = 0, compared = 0;
     while (true) {
-        if (tid == 0) s_part = atomicAdd(ticket, 1u);
+        if (tid == 0) {
+            const uint64_t p = atomicAdd(ticket, 1u);
+            s_p = p;
+            if (p < nparts) {
+                const uint64_t vb = p << pshift;
+                const uint32_t pv = uint32_t(nv_total - vb < P ? nv_total - vb : uint64_t(P));
+                const uint64_t tb = offs[vb], te = offs[vb + pv];
+                const uint64_t q0 = ppart[p], q1 = ppart[p + 1];
+                s_tb = tb; s_te = te; s_q0 = q0; s_q1 = q1;
+                s_kst = te - tb <= kcap;
+                s_pst = q1 - q0 <= pcap;
+                fence_proxy_async();
+                // three spans, one transaction barrier
+                const uintptr_t ao = reinterpret_cast<uintptr_t>(offs + vb);
+                const uintptr_t ak = reinterpret_cast<uintptr_t>(tkeys + tb);
+                const uintptr_t ae = reinterpret_cast<uintptr_t>(pin + q0);
+                auto span = [](uintptr_t a, size_t bytes, uint32_t& lo_off) -> uint32_t {
+                    const uintptr_t lo = a & ~uintptr_t(15), hi = (a + bytes + 15) & ~uintptr_t(15);
+                    lo_off = uint32_t(a - lo);
+                    return uint32_t(hi - lo);
+                };
+                uint32_t o0, o1 = 0, o2 = 0;
+                const uint32_t l0 = span(ao, size_t(pv + 1) * sizeof(OffT), o0);
+                const uint32_t l1 = s_kst ? span(ak, size_t(te - tb) * sizeof(K), o1) : 0;
+                const uint32_t l2 = s_pst ? span(ae, size_t(q1 - q0) * sizeof(PEnt), o2) : 0;
+                s_o0 = o0; s_o1 = o1; s_o2 = o2;
+                mbar_arrive_expect_tx(&s_bar, l0 + l1 + l2);
+                tma_load_1d(b_off, reinterpret_cast<const void*>(ao - o0), l0, &s_bar);
+                if (l1) tma_load_1d(b_key, reinterpret_cast<const void*>(ak - o1), l1, &s_bar);
+                if (l2) tma_load_1d(b_ent, reinterpret_cast<const void*>(ae - o2), l2, &s_bar);
+            }
+        }
         __syncthreads();
-        const uint64_t p = s_part;
+        const uint64_t p = s_p;
         if (p >= nparts) break;
         const uint64_t vb = p << pshift;
-        const uint32_t pv = uint32_t(nv_total - vb < P ? nv_total - vb : uint64_t(P));
-        const uint64_t tb = offs[vb], te = offs[vb + pv];
-        const uint64_t tn = te - tb;
-        const bool staged = tn <= kcap;
-        // relative offsets fit u32 whenever the slice is staged; unstaged
-        // slices fall back to 64-bit global offsets below
-        for (uint32_t j = tid; j <= pv; j += kPartProbeBlock) soff[j] = uint32_t(uint64_t(offs[vb + j]) - tb);
-        if (staged)
-            for (uint64_t j = tid; j < tn; j += kPartProbeBlock) skeys[j] = tkeys[tb + j];
-        __syncthreads();
-        const K* kp = staged ? skeys : tkeys + tb;
-        const uint64_t q0 = ppart[p], q1 = ppart[p + 1];
-        const uint64_t qn = q1 - q0;
+        const uint64_t tb = s_tb;
+        const uint64_t q0 = s_q0, qn = s_q1 - s_q0;
+        const OffT* soff = reinterpret_cast<const OffT*>(b_off + s_o0);
+        const K* kp = s_kst ? reinterpret_cast<const K*>(b_key + s_o1) : tkeys + tb;
+        const PEnt* ep = s_pst ? reinterpret_cast<const PEnt*>(b_ent + s_o2) : pin + q0;
+        mbar_wait(&s_bar, phase);
+        phase ^= 1;
         for (uint64_t base = uint64_t(warp) * 32; base < qn; base += uint64_t(nwarps) * 32) {
             const uint64_t i = base + lane;
             const bool valid = i < qn;
@@ -266,17 +318,12 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
             typename std::conditional<std::is_void<IT>::value, uint32_t, IT>::type pidx = 0;
             uint64_t b = 0, e = 0;
             if (valid) {
-                const auto ent = pin[q0 + i];
+                const auto ent = ep[i];
                 key = PE::key(ent);
                 if constexpr (PE::kHasVal) pidx = PE::val(ent);
                 const uint32_t lv = uint32_t(hv<POW2>(key, seed, hk, nv) - vb);
-                if (staged) {
-                    b = soff[lv];
-                    e = soff[lv + 1];
-                } else {
-                    b = uint64_t(offs[vb + lv]) - tb;
-                    e = uint64_t(offs[vb + lv + 1]) - tb;
-                }
+                b = uint64_t(soff[lv]) - tb;
+                e = uint64_t(soff[lv + 1]) - tb;
             }
             const uint64_t len = e - b;
             compared += len;
@@ -334,7 +381,7 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
         }
         __syncthreads();
     }
-    __shared__ unsigned long long s_m[kPartProbeBlock / 32], s_c[kPartProbeBlock / 32];
+    __shared__ unsigned long long s_m[nwarps], s_c[nwarps];
     matches = warp_sum(matches);
     compared = warp_sum(compared);
     if (lane == 0) {
@@ -372,8 +419,12 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
     constexpr uint32_t kTarget = 4096;
     const PartGeom g = make_geom(t.nv, t.n, 0, double(kTarget));
     const uint32_t P = 1u << g.pshift;
-    const uint32_t kcap = 3 * kTarget;
-    const size_t smem = ((size_t(P + 1) * 4 + 15) & ~size_t(15)) + size_t(kcap) * sizeof(K);
+    // table-key cap from the table's keys per partition, probe cap from the
+    // probes' expected count per partition (both ~1.5x the mean)
+    const double kmean = double(t.n) * double(P) / double(t.nv);
+    const double pmean = double(a.m) * double(P) / double(t.nv);
+    const uint32_t kcap = uint32_t(std::min(12288.0, std::max(512.0, 1.5 * kmean + 256)));
+    const uint32_t pcap = uint32_t(std::min(12288.0, std::max(512.0, 1.5 * pmean + 256)));
     const bool need_idx = a.counts != nullptr || a.pairs != nullptr;
     const int sms = num_sms();
     cudaError_t e;
@@ -417,6 +468,7 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
                                                static_cast<E0*>(reorg), s, "p_part_hist");
         }
         if (e != cudaSuccess) break;
+        const size_t smem = ProbeLayout<K, OffT, E1>::bytes(P, kcap, pcap);
         auto launch = [&](auto kern, const char* name, uint32_t* pc, const uint64_t* po, void* pr,
                           uint64_t cap) -> cudaError_t {
             cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -430,26 +482,27 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
             HG_LAUNCH(name, s,
                       kern<<<gk, kPartProbeBlock, smem, s>>>(
                           static_cast<const E1*>(reorg), ppart, g.nparts, t.nv, t.seed,
-                          t.hash_kind, nv, g.pshift, offs, tkeys, tvals, kcap, pc, po, pr, cap,
-                          a.totals, ticket));
+                          t.hash_kind, nv, g.pshift, offs, tkeys, tvals, kcap, pcap, pc, po, pr,
+                          cap, a.totals, ticket));
             return cudaGetLastError();
         };
         if (!need_idx) {
             // count-only: key-only entries
             auto kern = k_probe_part<K, VT, OffT, void, POW2, 0, false, uint32_t>;
+            const size_t smem0 = ProbeLayout<K, OffT, E0>::bytes(P, kcap, pcap);
             cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 int(smem));
+                                                 int(smem0));
             if (r != cudaSuccess) { e = r; break; }
             int per_sm = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPartProbeBlock, smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPartProbeBlock, smem0);
             const unsigned gk = unsigned(
                 std::min<uint64_t>(uint64_t(std::max(1, per_sm)) * sms, g.nparts));
             if ((e = cudaMemsetAsync(ticket, 0, 4, s)) != cudaSuccess) break;
             HG_LAUNCH("k8p_probe_part", s,
-                      kern<<<gk, kPartProbeBlock, smem, s>>>(
+                      kern<<<gk, kPartProbeBlock, smem0, s>>>(
                           static_cast<const E0*>(reorg), ppart, g.nparts, t.nv, t.seed,
-                          t.hash_kind, nv, g.pshift, offs, tkeys, tvals, kcap, nullptr, nullptr,
-                          nullptr, 0, a.totals, ticket));
+                          t.hash_kind, nv, g.pshift, offs, tkeys, tvals, kcap, pcap, nullptr,
+                          nullptr, nullptr, 0, a.totals, ticket));
             e = cudaGetLastError();
             break;
         }
@@ -498,8 +551,11 @@ static cudaError_t probe_impl(const TableDesc& t, const ProbeArgs& a, cudaStream
         return cudaSuccess;
     }
     const uint64_t table_bytes = (t.nv + 1) * sizeof(OffT) + t.n * sizeof(K);
-    const bool part = a.method == 2 || (a.method == 0 && table_bytes > (uint64_t(96) << 20) &&
-                                        a.m >= (uint64_t(1) << 20));
+    // partitioned probes need the partition's offsets slice in shared memory
+    const PartGeom pg = make_geom(t.nv, t.n, 0, 4096.0);
+    const bool fits = (size_t(1) << pg.pshift) * sizeof(OffT) <= size_t(64) << 10;
+    const bool part = fits && (a.method == 2 || (a.method == 0 && table_bytes > (uint64_t(96) << 20) &&
+                                                 a.m >= (uint64_t(1) << 20)));
     if (part) {
         if (a.m <= (uint64_t(1) << 32))
             return probe_partitioned<K, VT, OffT, uint32_t, POW2>(t, a, s);

@@ -168,9 +168,9 @@ k_part_hist(const K* __restrict__ keys, uint64_t n, uint64_t seed, int hk, Divis
 // ------------------------------------------------------------ multisplit
 
 constexpr int kSplitBlock = 512;
+constexpr int kSplitStages = 2;  // TMA input stages (one tile prefetched ahead)
 constexpr int kMaxDigits = 256;
-// 4096-entry tiles for <= 8-byte entries, 2048 for 16-byte ones (32 KB of
-// staging either way, so the kernel keeps 3-4 CTAs per SM).
+// 4096-entry tiles for <= 8-byte entries, 2048 for 16-byte ones.
 template <typename E>
 __host__ __device__ constexpr int split_items() { return sizeof(E) >= 16 ? 4 : 8; }
 template <typename E>
@@ -182,11 +182,11 @@ __host__ __device__ constexpr int split_tile() { return kSplitBlock * split_item
 // for digit d of a tile is reserved on cursor[cbase(tile) + d], where cbase is
 // 0 for pass 1 and (bucket << b2) for pass 2.
 // PASS2: tiles are laid out bucket by bucket; tile_prefix[b] = first tile of
-// high-digit bucket b (nb1 + 1 entries), bucket b spans
-// [part_start[b << b2], part_start[(b+1) << b2]).
-// Input tiles are double-buffered in shared memory with TMA 1-D bulk copies
-// (cp.async.bulk + mbarrier): tile i+1 streams in while tile i is ranked and
-// written, so HBM latency is off the critical path.
+// high-digit bucket b (nb1 + 1 entries, cached in shared memory), bucket b
+// spans [part_start[b << b2], part_start[(b+1) << b2]).
+// Input tiles are double-buffered in shared memory by TMA 1-D bulk copies
+// (cp.async.bulk + mbarrier): tile i+1 streams in while tile i is ranked,
+// staged digit-sorted in shared memory and written out in coalesced runs.
 template <typename K, typename VT, bool RAW>
 struct SplitLayout {
     using E = typename EntryT<K, VT>::T;
@@ -194,7 +194,7 @@ struct SplitLayout {
     static constexpr int kItems = split_items<E>();
     static constexpr int kTile = split_tile<E>();
     static constexpr size_t kInBytes = (size_t(kTile) * sizeof(InT) + 32 + 15) & ~size_t(15);
-    static constexpr size_t kBytes = 2 * kInBytes + size_t(kTile) * sizeof(E) + kTile;
+    static constexpr size_t kBytes = kSplitStages * kInBytes + size_t(kTile) * (sizeof(E) + 1);
 };
 
 template <typename K, typename VT, typename OffT, bool RAW, bool PASS2, bool POW2>
@@ -211,34 +211,39 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
     constexpr int kItems = L::kItems;
     constexpr int kTile = L::kTile;
     extern __shared__ __align__(128) unsigned char smem[];
-    unsigned char* const inb0 = smem;
-    unsigned char* const inb1 = smem + L::kInBytes;
-    E* const s_ent = reinterpret_cast<E*>(smem + 2 * L::kInBytes);
+    E* const s_ent = reinterpret_cast<E*>(smem + kSplitStages * L::kInBytes);
     uint8_t* const s_dig = reinterpret_cast<uint8_t*>(s_ent + kTile);
-    __shared__ uint64_t s_bar[2];
-    __shared__ uint64_t s_t0[2], s_t1[2], s_cb[2];
-    __shared__ uint32_t s_ofs[2], s_ok[2];
+    __shared__ uint64_t s_bar[kSplitStages];
+    __shared__ uint64_t s_t0[kSplitStages], s_t1[kSplitStages], s_cb[kSplitStages];
+    __shared__ uint32_t s_ofs[kSplitStages], s_ok[kSplitStages];
     __shared__ uint32_t s_cnt[kMaxDigits];
     __shared__ uint32_t s_off[kMaxDigits];
-    __shared__ OffT s_gb[kMaxDigits];
+    __shared__ uint64_t s_gbo[kMaxDigits];  // reserved global base - tile offset of each digit
     __shared__ uint32_t s_wsum[kSplitBlock / 32];
+    __shared__ uint64_t s_tp[PASS2 ? kMaxDigits + 1 : 1];  // tile_prefix cache
+    __shared__ uint64_t s_bs[PASS2 ? kMaxDigits + 1 : 1];  // bucket start cache
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t ndig = dmask + 1;
 
+    if constexpr (PASS2) {
+        for (uint32_t b = tid; b <= nb1; b += kSplitBlock) {
+            s_tp[b] = tile_prefix[b];
+            const uint64_t q = (uint64_t(b) << b2) < nparts ? (uint64_t(b) << b2) : nparts;
+            s_bs[b] = part_start[q];
+        }
+        __syncthreads();
+    }
     // (thread 0) range of a tile; false when past the last real tile
     auto tile_range = [&](uint64_t tile, uint64_t& t0, uint64_t& t1, uint64_t& cbase) -> bool {
         if constexpr (PASS2) {
-            if (tile >= tile_prefix[nb1]) return false;
+            if (tile >= s_tp[nb1]) return false;
             uint32_t lo = 0, hi = nb1;
             while (hi - lo > 1) {
                 const uint32_t mid = (lo + hi) >> 1;
-                if (tile_prefix[mid] <= tile) lo = mid; else hi = mid;
+                if (s_tp[mid] <= tile) lo = mid; else hi = mid;
             }
-            const uint64_t pe = (uint64_t(lo + 1) << b2) < nparts ? (uint64_t(lo + 1) << b2) : nparts;
-            const uint64_t bs = part_start[uint64_t(lo) << b2];
-            const uint64_t be = part_start[pe];
-            t0 = bs + (tile - tile_prefix[lo]) * kTile;
-            t1 = be < t0 + kTile ? be : t0 + kTile;
+            t0 = s_bs[lo] + (tile - s_tp[lo]) * kTile;
+            t1 = s_bs[lo + 1] < t0 + kTile ? s_bs[lo + 1] : t0 + kTile;
             cbase = uint64_t(lo) << b2;
         } else {
             if (tile >= ntiles) return false;
@@ -248,47 +253,60 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
         }
         return true;
     };
-    auto issue = [&](uint64_t tile, int buf) {
+    auto issue = [&](uint64_t tile, int st) {
         uint64_t t0 = 0, t1 = 0, cb = 0;
         const bool ok = tile_range(tile, t0, t1, cb);
-        s_ok[buf] = ok;
-        s_t0[buf] = t0;
-        s_t1[buf] = t1;
-        s_cb[buf] = cb;
+        s_ok[st] = ok;
+        s_t0[st] = t0;
+        s_t1[st] = t1;
+        s_cb[st] = cb;
         if (ok) {
             fence_proxy_async();
-            s_ofs[buf] = tma_load_span(buf ? inb1 : inb0, static_cast<const InT*>(in) + t0,
-                                       uint32_t((t1 - t0) * sizeof(InT)), &s_bar[buf]);
+            s_ofs[st] = tma_load_span(smem + st * L::kInBytes, static_cast<const InT*>(in) + t0,
+                                      uint32_t((t1 - t0) * sizeof(InT)), &s_bar[st]);
         }
     };
 
     if (tid == 0) {
-        mbar_init(&s_bar[0], 1);
-        mbar_init(&s_bar[1], 1);
+        for (int st = 0; st < kSplitStages; ++st) mbar_init(&s_bar[st], 1);
         fence_mbar_init();
-        issue(blockIdx.x, 0);
+        for (int st = 0; st < kSplitStages - 1; ++st) issue(blockIdx.x + uint64_t(st) * gridDim.x, st);
     }
     __syncthreads();
     uint64_t tile = blockIdx.x;
-    for (uint32_t it = 0;; ++it, tile += gridDim.x) {
-        const int buf = it & 1;
-        if (!s_ok[buf]) break;
-        if (tid == 0) issue(tile + gridDim.x, buf ^ 1);
-        const uint64_t t0 = s_t0[buf];
-        const uint32_t cnt = uint32_t(s_t1[buf] - t0);
-        const uint64_t cbase = s_cb[buf];
+    int st = 0;
+    uint32_t phase = 0;
+    for (;; tile += gridDim.x) {
+        if (!s_ok[st]) break;
+        // refill the stage consumed in the previous iteration
+        const int pf = st == 0 ? kSplitStages - 1 : st - 1;
+        if (tid == 0) issue(tile + uint64_t(kSplitStages - 1) * gridDim.x, pf);
+        const uint64_t t0 = s_t0[st];
+        const uint32_t cnt = uint32_t(s_t1[st] - t0);
+        const uint64_t cbase = s_cb[st];
         for (uint32_t d = tid; d < ndig; d += kSplitBlock) s_cnt[d] = 0;
-        mbar_wait(&s_bar[buf], (it >> 1) & 1);
-        const InT* src = reinterpret_cast<const InT*>((buf ? inb1 : inb0) + s_ofs[buf]);
+        mbar_wait(&s_bar[st], phase);
+        const InT* src = reinterpret_cast<const InT*>(smem + st * L::kInBytes + s_ofs[st]);
         __syncthreads();
 
+        E ent[kItems];
         uint32_t dr[kItems];  // digit << 16 | rank
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
             const uint32_t j = tid + k * kSplitBlock;
             if (j < cnt) {
                 K key;
-                if constexpr (RAW) key = src[j]; else key = ET::key(src[j]);
+                if constexpr (RAW) {
+                    key = src[j];
+                    if constexpr (ET::kHasVal) {
+                        ent[k] = ET::make(key, vals ? VT(vals[t0 + j]) : VT(t0 + j));
+                    } else {
+                        ent[k] = ET::make(key, 0);
+                    }
+                } else {
+                    ent[k] = src[j];
+                    key = ET::key(ent[k]);
+                }
                 const uint32_t p = uint32_t(hv<POW2>(key, seed, hk, nv) >> pshift);
                 const uint32_t d = (p >> dshift) & dmask;
                 dr[k] = (d << 16) | atomicAdd(s_cnt + d, 1u);
@@ -308,8 +326,9 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
         if (tid < ndig) {
             uint32_t base = 0;
             for (uint32_t w = 0; w < warp; ++w) base += s_wsum[w];
-            s_off[tid] = base + inc - c;
-            if (c) s_gb[tid] = atom_add(cursor + cbase + tid, OffT(c));
+            const uint32_t off = base + inc - c;
+            s_off[tid] = off;
+            if (c) s_gbo[tid] = uint64_t(atom_add(cursor + cbase + tid, OffT(c))) - off;
         }
         __syncthreads();
 #pragma unroll
@@ -318,16 +337,7 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
             if (j < cnt) {
                 const uint32_t d = dr[k] >> 16;
                 const uint32_t slot = s_off[d] + (dr[k] & 0xFFFFu);
-                if constexpr (RAW) {
-                    const K key = src[j];
-                    if constexpr (ET::kHasVal) {
-                        s_ent[slot] = ET::make(key, vals ? VT(vals[t0 + j]) : VT(t0 + j));
-                    } else {
-                        s_ent[slot] = ET::make(key, 0);
-                    }
-                } else {
-                    s_ent[slot] = src[j];
-                }
+                s_ent[slot] = ent[k];
                 s_dig[slot] = uint8_t(d);
             }
         }
@@ -335,12 +345,13 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
             const uint32_t j = tid + k * kSplitBlock;
-            if (j < cnt) {
-                const uint32_t d = s_dig[j];
-                out[uint64_t(s_gb[d]) + (j - s_off[d])] = s_ent[j];
-            }
+            if (j < cnt) out[s_gbo[s_dig[j]] + j] = s_ent[j];
         }
         __syncthreads();
+        if (++st == kSplitStages) {
+            st = 0;
+            phase ^= 1;
+        }
     }
 }
 
