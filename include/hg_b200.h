@@ -67,6 +67,12 @@ typedef struct hg_build_config {
     int32_t stable;              /* 1 = ExecMode::sequential layout: segments in input order */
     int32_t aggregate;           /* warp-aggregated atomics: -1 auto, 0 off, 1 on */
     uint64_t partition_vertices; /* binned build partition width (power of two); 0 = auto */
+    /* Hash-range shard (multi-GPU): when global_vertices != 0
+     * the table holds global vertices [vertex_base, vertex_base + vertex_count)
+     * of a V = global_vertices table; vertex v is stored as local v - vertex_base.
+     * Keys must have been routed to this shard (hg_route). */
+    uint64_t global_vertices;
+    uint64_t vertex_base;
 } hg_build_config;
 
 /* Defaults of BuildConfig{} (core.hpp:30-35): load 1.0, bins 2^15, seed 0,
@@ -156,6 +162,22 @@ hg_status hg_count_instances(const hg_table* t, uint64_t key, uint64_t* out, voi
  * the code of the first violated invariant (see hg_util.cu). */
 hg_status hg_validate(const hg_table* t, const void* input_keys, uint64_t expected_entries,
                       int32_t* violation, void* stream);
+
+/* Multi-GPU routing (K11). Shard g of G owns global vertices
+ * [g*S, min((g+1)*S, V)), S = ceil(V/G) (the reference's bin formula,
+ * core.hpp:192-197, at bins = G). */
+hg_status hg_shard_range(uint64_t global_vertices, uint32_t shards, uint32_t shard,
+                         uint64_t* vertex_base, uint64_t* vertex_count);
+
+/* Groups n device-resident keys by owner shard into SoA device buffers
+ * out_keys/out_vals (n entries each, keys of shard 0 first) and writes the
+ * per-shard counts to shard_counts (G entries; host or device). Values are
+ * vals[i] or, when vals is NULL, val_base + i (global input positions) of
+ * width val_width. G <= 256. */
+hg_status hg_route(const void* keys, int32_t key_width, const void* vals, int32_t val_width,
+                   uint64_t n, uint64_t val_base, uint64_t hash_seed, int32_t hash_kind,
+                   uint64_t global_vertices, uint32_t shards, void* out_keys, void* out_vals,
+                   uint64_t* shard_counts, void* stream);
 
 /* Synthetic inputs: kind 0 = (u32|u64)splitmix64(seed, start+i);
  * kind 1 = C4 probes with hit ratio `hit` over ref[n_ref]; kind 2 = scramble31(start+i). */

@@ -49,6 +49,12 @@ uint64_t hgo_hash_to_vertex(uint64_t key, uint64_t seed, uint64_t nv) {
     return hgo_vertex(key, seed, nv, HGO_HASH_MIX64);
 }
 
+/* Vectorised hash_to_vertex over an array (test convenience). */
+void hgo_vertices(const uint64_t* keys, uint64_t n, uint64_t seed, uint64_t nv, int hash_kind,
+                  uint64_t* out) {
+    for (uint64_t i = 0; i < n; ++i) out[i] = hgo_vertex(keys[i], seed, nv, hash_kind);
+}
+
 /* core.hpp:59-63 derived_vertex_count: max(1, floor(n / load)) in double. */
 int hgo_derived_vertex_count(uint64_t n, double load, uint64_t* out) {
     if (!(load > 0.0)) return HGO_EINVAL;

@@ -82,6 +82,8 @@ class Oracle:
         lib.hgo_vertex.argtypes = [u64, u64, u64, i32]
         lib.hgo_hash_to_vertex.restype = u64
         lib.hgo_hash_to_vertex.argtypes = [u64, u64, u64]
+        lib.hgo_vertices.restype = None
+        lib.hgo_vertices.argtypes = [_P, u64, u64, u64, i32, _P]
         lib.hgo_derived_vertex_count.restype = i32
         lib.hgo_derived_vertex_count.argtypes = [u64, dbl, _P]
         lib.hgo_build_v1.restype = i32
@@ -120,6 +122,12 @@ class Oracle:
 
     def vertex(self, key: int, seed: int, nv: int, hash_kind: int = HASH_MIX64) -> int:
         return int(self.lib.hgo_vertex(key, seed, nv, hash_kind))
+
+    def vertices(self, keys, seed: int, nv: int, hash_kind: int = HASH_MIX64) -> np.ndarray:
+        keys = _u64(keys)
+        out = np.zeros(len(keys), np.uint64)
+        self.lib.hgo_vertices(_ptr(keys), len(keys), seed, nv, hash_kind, _ptr(out))
+        return out
 
     def derived_vertex_count(self, n: int, load: float) -> int:
         out = np.zeros(1, np.uint64)

@@ -30,6 +30,8 @@ class hg_build_config(C.Structure):
         ("stable", C.c_int32),
         ("aggregate", C.c_int32),
         ("partition_vertices", C.c_uint64),
+        ("global_vertices", C.c_uint64),
+        ("vertex_base", C.c_uint64),
     ]
 
 
@@ -101,6 +103,9 @@ SIGNATURES = {
     "hg_count_instances": (_i32, [_vp, _u64, C.POINTER(_u64), _vp]),
     "hg_validate": (_i32, [_vp, _vp, _u64, C.POINTER(_i32), _vp]),
     "hg_generate": (_i32, [_vp, _i32, _u64, _i32, _u64, _u64, C.c_double, _vp, _u64, _vp]),
+    "hg_shard_range": (_i32, [_u64, C.c_uint32, C.c_uint32, C.POINTER(_u64), C.POINTER(_u64)]),
+    "hg_route": (_i32, [_vp, _i32, _vp, _i32, _u64, _u64, _u64, _i32, _u64, C.c_uint32, _vp, _vp,
+                        _vp, _vp]),
     "hg_profiler_enable": (None, [_i32]),
     "hg_profiler_collect": (_i32, [C.POINTER(hg_kernel_time), _i32]),
 }

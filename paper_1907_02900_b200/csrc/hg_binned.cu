@@ -159,7 +159,7 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
         const bool vec4 = per == 4 && j1 - j0 == 4;
         uint4 c4 = make_uint4(0, 0, 0, 0);
         if (vec4) {
-            c4 = *reinterpret_cast<const uint4*>(cnt + j0);
+            c4 = lds128(cnt + j0);
             run = c4.x + c4.y + c4.z + c4.w;
         } else {
             for (uint32_t j = j0; j < j1; ++j) run += cnt[j];
@@ -186,7 +186,7 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
         uint32_t acc = s_warp[warp] + inc - run;
         if (vec4) {
             const uint4 st = make_uint4(acc, acc + c4.x, acc + c4.x + c4.y, acc + c4.x + c4.y + c4.z);
-            *reinterpret_cast<uint4*>(cnt + j0) = st;
+            sts128(cnt + j0, st);
             if constexpr (sizeof(OffT) == 4) {
                 // offs + 1 is 16-byte aligned (hg_capi pads it) and vb + j0 is a multiple of 4
                 *reinterpret_cast<uint4*>(offs + vb + j0 + 1) =
@@ -244,7 +244,7 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
 template <typename K, typename VT, typename OffT, bool POW2>
 cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s) {
     using E = typename EntryT<K, VT>::T;
-    const Divisor nv = make_divisor(t.nv);
+    const Divisor nv = make_divisor(global_nv(t), t.vbase);
     OffT* offs = static_cast<OffT*>(t.offs);
     cudaError_t e;
     if (t.n == 0) return cudaMemsetAsync(offs, 0, (t.nv + 1) * sizeof(OffT), s);

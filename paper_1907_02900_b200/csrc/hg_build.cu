@@ -258,7 +258,7 @@ static cudaError_t stable_order(const TableDesc& t, cudaStream_t s) {
 
 template <typename K, typename VT, typename OffT, bool POW2>
 static cudaError_t build_v1_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s) {
-    const Divisor nv = make_divisor(t.nv);
+    const Divisor nv = make_divisor(global_nv(t), t.vbase);
     OffT* offs = static_cast<OffT*>(t.offs);
     cudaError_t e = cudaMemsetAsync(offs, 0, (t.nv + 1) * sizeof(OffT), s);
     if (e != cudaSuccess || t.n == 0) return e;
@@ -285,7 +285,8 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
 
 template <typename K, typename VT, typename OffT>
 static cudaError_t build_typed(const TableDesc& t, const BuildArgs& a, cudaStream_t s) {
-    const bool pow2 = (t.nv & (t.nv - 1)) == 0;
+    const uint64_t gv = global_nv(t);
+    const bool pow2 = (gv & (gv - 1)) == 0;
     cudaError_t e;
     if (a.variant == 2) {
         e = pow2 ? build_v2_impl<K, VT, OffT, true>(t, a, s)

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -165,6 +166,8 @@ void hg_build_config_init(hg_build_config* cfg) {
     cfg->stable = 0;
     cfg->aggregate = -1;
     cfg->partition_vertices = 0;
+    cfg->global_vertices = 0;
+    cfg->vertex_base = 0;
 }
 
 void hg_probe_options_init(hg_probe_options* o) {
@@ -214,6 +217,11 @@ hg_status hg_build(const void* keys, int32_t key_width, const void* vals, int32_
         return fail(HG_EINVAL, "unknown hash_kind");
     if (n && !keys) return fail(HG_EINVAL, "keys is NULL");
     uint64_t nv = cfg.vertex_count;
+    if (cfg.global_vertices) {
+        if (!nv) return fail(HG_EINVAL, "a shard build needs vertex_count (its local vertex range)");
+        if (cfg.vertex_base + nv > cfg.global_vertices)
+            return fail(HG_EINVAL, "shard vertex range exceeds global_vertices");
+    }
     if (!nv) {
         hg_status st = hg_derived_vertex_count(n, cfg.load_factor, &nv);
         if (st != HG_OK) return st;
@@ -232,6 +240,8 @@ hg_status hg_build(const void* keys, int32_t key_width, const void* vals, int32_
     hg::TableDesc& d = t->d;
     d.nv = nv;
     d.n = n;
+    d.gnv = cfg.global_vertices;
+    d.vbase = cfg.global_vertices ? cfg.vertex_base : 0;
     d.seed = cfg.hash_seed;
     d.hash_kind = cfg.hash_kind;
     d.key_bytes = key_width;
@@ -473,6 +483,50 @@ hg_status hg_validate(const hg_table* t, const void* input_keys, uint64_t expect
     // input size), which the reference tests right after 5.
     if (code > 6 && t->d.n != expected_entries) code = 6;
     *violation = int32_t(code);
+    return HG_OK;
+}
+
+hg_status hg_shard_range(uint64_t global_vertices, uint32_t shards, uint32_t shard,
+                         uint64_t* vertex_base, uint64_t* vertex_count) {
+    if (!vertex_base || !vertex_count) return fail(HG_EINVAL, "NULL argument");
+    if (shards < 1 || shard >= shards || global_vertices < 1)
+        return fail(HG_EINVAL, "need 0 <= shard < shards and global_vertices >= 1");
+    const uint64_t span = (global_vertices + shards - 1) / shards;
+    const uint64_t b = std::min<uint64_t>(global_vertices, uint64_t(shard) * span);
+    const uint64_t e = std::min<uint64_t>(global_vertices, b + span);
+    *vertex_base = b;
+    *vertex_count = e - b;
+    return HG_OK;
+}
+
+hg_status hg_route(const void* keys, int32_t key_width, const void* vals, int32_t val_width,
+                   uint64_t n, uint64_t val_base, uint64_t hash_seed, int32_t hash_kind,
+                   uint64_t global_vertices, uint32_t shards, void* out_keys, void* out_vals,
+                   uint64_t* shard_counts, void* stream) {
+    if (key_width != 4 && key_width != 8) return fail(HG_EINVAL, "key_width must be 4 or 8");
+    if (val_width != 4 && val_width != 8) return fail(HG_EINVAL, "val_width must be 4 or 8");
+    if (shards < 1 || shards > 256) return fail(HG_EINVAL, "shards must be in [1, 256]");
+    if (global_vertices < 1) return fail(HG_EINVAL, "global_vertices must be >= 1");
+    if (hash_kind != HG_HASH_MIX64 && hash_kind != HG_HASH_IDENTITY)
+        return fail(HG_EINVAL, "unknown hash_kind");
+    if (!shard_counts) return fail(HG_EINVAL, "shard_counts is NULL");
+    if (n && (!is_device_ptr(keys) || !is_device_ptr(out_keys) || !is_device_ptr(out_vals) ||
+              (vals && !is_device_ptr(vals))))
+        return fail(HG_EINVAL, "hg_route takes device buffers");
+    int dev = 0;
+    if (hg_status st = need_device(&dev); st != HG_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool counts_dev = is_device_ptr(shard_counts);
+    uint64_t* dc = shard_counts;
+    if (!counts_dev) HG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dc), shards * 8, s));
+    cudaError_t e = hg::route_keys(keys, key_width, vals, val_width, n, val_base, hash_seed,
+                                   hash_kind, global_vertices, shards, out_keys, out_vals, dc, s);
+    if (e == cudaSuccess && !counts_dev) {
+        e = cudaMemcpyAsync(shard_counts, dc, shards * 8, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    }
+    if (!counts_dev) cudaFreeAsync(dc, s);
+    if (e != cudaSuccess) return cuda_fail(e, "hg_route");
     return HG_OK;
 }
 

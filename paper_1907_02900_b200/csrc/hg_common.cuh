@@ -18,20 +18,25 @@ enum HashKind : int { kHashMix64 = 0, kHashIdentity = 1 };
 // estimate q = umulhi(h, magic) satisfies q_true-1 <= q <= q_true for every
 // h < 2^64 (error h*(1/d - magic/2^64) <= h/2^64 < 1), so one correction
 // step is exact. Power-of-two divisors use shift/mask (template POW2).
+// For the vertex space, `base` is subtracted after the reduction: a
+// hash-range shard owning global vertices [base, base + local V) numbers its
+// vertices locally; base = 0 for an unsharded table.
 struct Divisor {
     uint64_t d;
     uint64_t magic;
     uint32_t shift;  // log2(d) when d is a power of two
     uint32_t pow2;
+    uint64_t base;
 };
 
-inline Divisor make_divisor(uint64_t d) {
+inline Divisor make_divisor(uint64_t d, uint64_t base = 0) {
     Divisor r;
     r.d = d;
     r.magic = ~uint64_t(0) / d;
     r.pow2 = (d & (d - 1)) == 0;
     r.shift = 0;
     while (r.pow2 && (uint64_t(1) << r.shift) < d) ++r.shift;
+    r.base = base;
     return r;
 }
 
@@ -73,9 +78,9 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
 template <int HK, bool POW2>
 __device__ __forceinline__ uint64_t vertex_of(uint64_t key, uint64_t seed, const Divisor& nv) {
     if constexpr (HK == kHashIdentity) {
-        return mod_of<POW2>(key, nv);
+        return mod_of<POW2>(key, nv) - nv.base;
     } else {
-        return mod_of<POW2>(mix64(key ^ seed), nv);
+        return mod_of<POW2>(mix64(key ^ seed), nv) - nv.base;
     }
 }
 
@@ -215,6 +220,20 @@ __device__ __forceinline__ uint32_t tma_load_span(void* dst, const void* src, ui
     mbar_arrive_expect_tx(bar, len);
     if (len) tma_load_1d(dst, reinterpret_cast<const void*>(lo), len, bar);
     return uint32_t(a - lo);
+}
+
+__device__ __forceinline__ uint4 lds128(const void* p) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(smem_addr(p)));
+    return v;
+}
+
+__device__ __forceinline__ void sts128(void* p, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(smem_addr(p)), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
 }
 
 __device__ __forceinline__ uint32_t atom_add(uint32_t* p, uint32_t v) { return atomicAdd(p, v); }

@@ -411,7 +411,7 @@ __global__ void k_scatter_counts(const typename EntryT<K, IT>::T* __restrict__ p
 
 template <typename K, typename VT, typename OffT, typename IT, bool POW2>
 static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cudaStream_t s) {
-    const Divisor nv = make_divisor(t.nv);
+    const Divisor nv = make_divisor(global_nv(t), t.vbase);
     const OffT* offs = static_cast<const OffT*>(t.offs);
     const K* tkeys = static_cast<const K*>(t.keys);
     const VT* tvals = static_cast<const VT*>(t.vals);
@@ -542,7 +542,7 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
 
 template <typename K, typename VT, typename OffT, bool POW2>
 static cudaError_t probe_impl(const TableDesc& t, const ProbeArgs& a, cudaStream_t s) {
-    const Divisor nv = make_divisor(t.nv);
+    const Divisor nv = make_divisor(global_nv(t), t.vbase);
     const OffT* offs = static_cast<const OffT*>(t.offs);
     const K* probes = static_cast<const K*>(a.probes);
     const K* tkeys = static_cast<const K*>(t.keys);
@@ -608,7 +608,8 @@ static cudaError_t probe_impl(const TableDesc& t, const ProbeArgs& a, cudaStream
 
 template <typename K, typename VT, typename OffT>
 static cudaError_t probe_pow(const TableDesc& t, const ProbeArgs& a, cudaStream_t s) {
-    return (t.nv & (t.nv - 1)) == 0 ? probe_impl<K, VT, OffT, true>(t, a, s)
+    const uint64_t gv = global_nv(t);
+    return (gv & (gv - 1)) == 0 ? probe_impl<K, VT, OffT, true>(t, a, s)
                                     : probe_impl<K, VT, OffT, false>(t, a, s);
 }
 template <typename K, typename VT>

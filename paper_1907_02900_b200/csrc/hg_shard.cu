@@ -1,0 +1,169 @@
+// hg_shard.cu -- hash-range routing for the multi-GPU (sharded) table.
+//
+// The reference partitions its vertex range only for cache locality
+// (core.hpp:192-197, bin = v / ceil(V / bins)); with G GPUs the same formula
+// at bins = G picks the owner GPU: owner(v) = v / ceil(V/G).
+// K11 (this file) groups a GPU's keys by owner so that one NCCL all-to-all
+// (torch.distributed over NVLink) moves every key to the GPU that builds /
+// probes its vertex range:
+//   k_route_hist     per-owner counts (shared-memory histogram, G <= 256)
+//   scan             owner starts
+//   k_route_scatter  per 4096-key tile: shared-memory rank by owner, one
+//                    global atomic per (tile, owner) reserving a run, then
+//                    the tile is staged owner-sorted and written as coalesced
+//                    runs into SoA keys[] / vals[] send buffers.
+#include <algorithm>
+
+#include "hg_common.cuh"
+#include "hg_internal.h"
+#include "hg_scan.cuh"
+
+namespace hg {
+
+constexpr int kRouteBlock = 512;
+constexpr int kRouteItems = 4;
+constexpr int kRouteTile = kRouteBlock * kRouteItems;
+
+template <bool POW2>
+__device__ __forceinline__ uint32_t owner_of(uint64_t key, uint64_t seed, int hk, const Divisor& gv,
+                                             const Divisor& span) {
+    const uint64_t v = hk == kHashIdentity ? vertex_of<kHashIdentity, POW2>(key, seed, gv)
+                                           : vertex_of<kHashMix64, POW2>(key, seed, gv);
+    return uint32_t(div_of<false>(v, span));
+}
+
+template <typename K, bool POW2>
+__global__ void __launch_bounds__(kRouteBlock)
+k_route_hist(const K* __restrict__ keys, uint64_t n, uint64_t seed, int hk, Divisor gv,
+             Divisor span, uint32_t shards, unsigned long long* __restrict__ counts) {
+    __shared__ uint32_t sh[256];
+    for (uint32_t i = threadIdx.x; i < shards; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        atomicAdd(sh + owner_of<POW2>(keys[i], seed, hk, gv, span), 1u);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < shards; i += blockDim.x)
+        if (sh[i]) atomicAdd(counts + i, (unsigned long long)sh[i]);
+}
+
+template <typename K, typename VT, bool POW2>
+__global__ void __launch_bounds__(kRouteBlock)
+k_route_scatter(const K* __restrict__ keys, const VT* __restrict__ vals, uint64_t n,
+                uint64_t val_base, uint64_t seed, int hk, Divisor gv, Divisor span,
+                uint32_t shards, unsigned long long* __restrict__ cursor, K* __restrict__ okeys,
+                VT* __restrict__ ovals) {
+    __shared__ K s_k[kRouteTile];
+    __shared__ VT s_v[kRouteTile];
+    __shared__ uint8_t s_o[kRouteTile];
+    __shared__ uint32_t s_cnt[256], s_off[256];
+    __shared__ unsigned long long s_gbo[256];
+    const uint32_t tid = threadIdx.x;
+    const uint64_t ntiles = (n + kRouteTile - 1) / kRouteTile;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t t0 = tile * kRouteTile;
+        const uint32_t cnt = uint32_t(n - t0 < kRouteTile ? n - t0 : kRouteTile);
+        for (uint32_t d = tid; d < shards; d += kRouteBlock) s_cnt[d] = 0;
+        __syncthreads();
+        K kk[kRouteItems];
+        uint32_t orank[kRouteItems];
+#pragma unroll
+        for (int k = 0; k < kRouteItems; ++k) {
+            const uint32_t j = tid + k * kRouteBlock;
+            if (j < cnt) {
+                kk[k] = keys[t0 + j];
+                const uint32_t o = owner_of<POW2>(kk[k], seed, hk, gv, span);
+                orank[k] = (o << 16) | atomicAdd(s_cnt + o, 1u);
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t acc = 0;
+            for (uint32_t d = 0; d < shards; ++d) {
+                const uint32_t c = s_cnt[d];
+                s_off[d] = acc;
+                if (c) s_gbo[d] = atomicAdd(cursor + d, (unsigned long long)c) - acc;
+                acc += c;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kRouteItems; ++k) {
+            const uint32_t j = tid + k * kRouteBlock;
+            if (j < cnt) {
+                const uint32_t o = orank[k] >> 16;
+                const uint32_t slot = s_off[o] + (orank[k] & 0xFFFFu);
+                s_k[slot] = kk[k];
+                s_v[slot] = vals ? vals[t0 + j] : VT(val_base + t0 + j);
+                s_o[slot] = uint8_t(o);
+            }
+        }
+        __syncthreads();
+        for (uint32_t j = tid; j < cnt; j += kRouteBlock) {
+            const uint64_t dst = s_gbo[s_o[j]] + j;
+            okeys[dst] = s_k[j];
+            ovals[dst] = s_v[j];
+        }
+        __syncthreads();
+    }
+}
+
+template <typename K, typename VT, bool POW2>
+static cudaError_t route_typed(const void* keys, const void* vals, uint64_t n, uint64_t val_base,
+                               uint64_t seed, int hk, uint64_t V, uint32_t G, void* out_keys,
+                               void* out_vals, uint64_t* shard_counts, cudaStream_t s) {
+    const Divisor gv = make_divisor(V);
+    const Divisor span = make_divisor((V + G - 1) / G);
+    auto* counts = reinterpret_cast<unsigned long long*>(shard_counts);
+    cudaError_t e = cudaMemsetAsync(counts, 0, G * 8, s);
+    if (e != cudaSuccess || n == 0) return e;
+    const int sms = num_sms();
+    const unsigned gh = unsigned(std::min<uint64_t>((n + kRouteBlock - 1) / kRouteBlock, uint64_t(sms) * 4));
+    HG_LAUNCH("k11_route_hist", s,
+              k_route_hist<K, POW2><<<gh, kRouteBlock, 0, s>>>(static_cast<const K*>(keys), n, seed,
+                                                               hk, gv, span, G, counts));
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // cursor[d] = exclusive prefix of counts
+    unsigned long long* cursor = nullptr;
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&cursor), (G + 1) * 8 + 256 +
+                                                                  scan_scratch_bytes(G), s)) != cudaSuccess)
+        return e;
+    void* scr = reinterpret_cast<char*>(cursor) + ((G + 1) * 8 + 255) / 256 * 256;
+    e = launch_scan<unsigned long long, unsigned long long>(counts, cursor, G, scr, nullptr, s,
+                                                            "route_scan");
+    if (e == cudaSuccess) {
+        const uint64_t tiles = (n + kRouteTile - 1) / kRouteTile;
+        const unsigned gs = unsigned(std::min<uint64_t>(tiles, uint64_t(sms) * 2));
+        HG_LAUNCH("k11_route_scatter", s,
+                  (k_route_scatter<K, VT, POW2><<<gs, kRouteBlock, 0, s>>>(
+                      static_cast<const K*>(keys), static_cast<const VT*>(vals), n, val_base, seed,
+                      hk, gv, span, G, cursor, static_cast<K*>(out_keys),
+                      static_cast<VT*>(out_vals))));
+        e = cudaGetLastError();
+    }
+    cudaFreeAsync(cursor, s);
+    return e;
+}
+
+cudaError_t route_keys(const void* keys, int key_bytes, const void* vals, int val_bytes,
+                       uint64_t n, uint64_t val_base, uint64_t seed, int hash_kind,
+                       uint64_t global_vertices, uint32_t shards, void* out_keys, void* out_vals,
+                       uint64_t* shard_counts, cudaStream_t s) {
+    const bool pow2 = (global_vertices & (global_vertices - 1)) == 0;
+#define HG_ROUTE(K, VT)                                                                        \
+    return pow2 ? route_typed<K, VT, true>(keys, vals, n, val_base, seed, hash_kind,           \
+                                           global_vertices, shards, out_keys, out_vals,        \
+                                           shard_counts, s)                                    \
+                : route_typed<K, VT, false>(keys, vals, n, val_base, seed, hash_kind,          \
+                                            global_vertices, shards, out_keys, out_vals,       \
+                                            shard_counts, s)
+    if (key_bytes == 4) {
+        if (val_bytes == 4) HG_ROUTE(uint32_t, uint32_t);
+        HG_ROUTE(uint32_t, uint64_t);
+    }
+    if (val_bytes == 4) HG_ROUTE(uint64_t, uint32_t);
+    HG_ROUTE(uint64_t, uint64_t);
+#undef HG_ROUTE
+}
+
+}  // namespace hg

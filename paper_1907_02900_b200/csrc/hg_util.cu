@@ -131,9 +131,9 @@ static cudaError_t validate_typed(const TableDesc& t, const void* input, uint32_
                                   cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(d_code, 0xff, 4, s);
     if (e != cudaSuccess) return e;
-    const Divisor dv = make_divisor(t.nv);
+    const Divisor dv = make_divisor(global_nv(t), t.vbase);
     const unsigned grid = unsigned(num_sms()) * 8;
-    if ((t.nv & (t.nv - 1)) == 0) {
+    if ((global_nv(t) & (global_nv(t) - 1)) == 0) {
         k_validate_vertices<K, VT, OffT, true><<<grid, 256, 0, s>>>(
             static_cast<const OffT*>(t.offs), t.nv, t.n, t.seed, t.hash_kind, dv,
             static_cast<const K*>(t.keys), d_code);

@@ -309,7 +309,7 @@ def _hash_kind(hasher) -> int:
 
 
 def _build(variant: int, keys, cfg: Optional[BuildConfig], hasher, stats, vertex_count,
-           vals=None, stream=None) -> HashGraph:
+           vals=None, stream=None, shard=None) -> HashGraph:
     cfg = cfg or BuildConfig()
     ka = _Arr(keys)
     va = _Arr(vals) if vals is not None else None
@@ -324,6 +324,8 @@ def _build(variant: int, keys, cfg: Optional[BuildConfig], hasher, stats, vertex
     c.stable = 1 if cfg.mode == ExecMode.sequential else 0
     c.aggregate = int(cfg.aggregate)
     c.partition_vertices = int(cfg.partition_vertices)
+    if shard is not None:
+        c.global_vertices, c.vertex_base = int(shard[0]), int(shard[1])
     s = stream if stream is not None else _stream_for(ka, va)
     h = C.c_void_p()
     _check(_lib.lib().hg_build(ka.ptr, ka.width, va.ptr if va else None, va.width if va else 0,
@@ -344,16 +346,19 @@ def _build(variant: int, keys, cfg: Optional[BuildConfig], hasher, stats, vertex
 
 def build_v1(keys, cfg: Optional[BuildConfig] = None, stats: Optional[BuildStats] = None,
              vertex_count: Optional[int] = None, hasher=None, vals=None,
-             stream=None) -> HashGraph:
-    """core.hpp:160-177 (simple build: count, scan, place)."""
-    return _build(BUILD_SIMPLE, keys, cfg, hasher, stats, vertex_count, vals, stream)
+             stream=None, shard=None) -> HashGraph:
+    """core.hpp:160-177 (simple build: count, scan, place).
+    vals: explicit entry values (default: input positions, Entry::index).
+    shard: (global_vertices, vertex_base) for a hash-range shard whose local
+    vertex range has vertex_count vertices (sharded.py)."""
+    return _build(BUILD_SIMPLE, keys, cfg, hasher, stats, vertex_count, vals, stream, shard)
 
 
 def build_v2(keys, cfg: Optional[BuildConfig] = None, stats: Optional[BuildStats] = None,
              vertex_count: Optional[int] = None, hasher=None, vals=None,
-             stream=None) -> HashGraph:
+             stream=None, shard=None) -> HashGraph:
     """core.hpp:183-230 (binned build: partition, then per-partition build)."""
-    return _build(BUILD_BINNED, keys, cfg, hasher, stats, vertex_count, vals, stream)
+    return _build(BUILD_BINNED, keys, cfg, hasher, stats, vertex_count, vals, stream, shard)
 
 
 def probe_standard(hg: HashGraph, probe_keys, opts: Optional[ProbeOptions] = None,

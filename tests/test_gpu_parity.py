@@ -328,3 +328,57 @@ def test_large_scale_vs_oracle(oracle, cuda, log2n, width, load):
     res = torch.zeros(2, dtype=torch.int64, device="cuda")
     hg.probe_device(t, dhalf, res, method=2)
     assert [int(x) for x in res.cpu()] == [ro["match_count"], ro["key_comparisons"]]
+
+
+@pytest.mark.parametrize("G,load,variant", [(4, 1.0, 2), (3, 1.5, 1), (8, 0.5, 2)])
+def test_shard_route_and_local_builds(oracle, cuda, G, load, variant):
+    """Single-GPU run of the sharded path's device kernels: hg_route groups
+    keys by owner shard, every shard builds its vertex range with the global
+    hash (vertex_base), and the concatenated shards equal the oracle table;
+    routed probes summed over shards equal the oracle's totals."""
+    torch = cuda
+    from paper_1907_02900_b200.sharded import CudaEngine, shard_range
+    n = 200_000
+    keys = torch.empty(n, dtype=torch.int32, device="cuda")
+    hg.generate(keys, kind=0, seed=21)
+    hk = keys.cpu().numpy().view(np.uint32).astype(np.uint64)
+    V = hg.derived_vertex_count(n, load)
+    ref = oracle.build(hk, 1, load)
+    eng = CudaEngine(variant)
+    sk, sv, counts = eng.route(keys, None, 4, 1000, 0, 0, V, G)
+    counts = counts.cpu().tolist()
+    assert sum(counts) == n
+    offs_all, k_all, v_all = [np.zeros(1, np.uint64)], [], []
+    start = 0
+    edge_base = 0
+    for g in range(G):
+        base, cnt = shard_range(V, G, g)
+        kk, vv = sk[start:start + counts[g]], sv[start:start + counts[g]]
+        start += counts[g]
+        t = eng.build(kk, vv, V, base, max(cnt, 1), BuildConfig(load_factor=load,
+                                                             mode=ExecMode.sequential), 0)
+        assert t.num_vertices() == max(cnt, 1)
+        offs_all.append(t.offsets()[1:] + edge_base)
+        edge_base += t.num_edges()
+        k_all.append(t.edge_keys())
+        v_all.append(t.edge_index())
+    offs = np.concatenate(offs_all)
+    assert (offs == ref.offsets).all()
+    # values carry global positions (val_base = 1000); sequential -> exact order
+    assert (np.concatenate(k_all) == ref.keys).all()
+    assert (np.concatenate(v_all) == ref.index + 1000).all()
+    # probes: route, probe each shard, sum
+    probes = torch.cat([keys[: n // 2], keys[: n // 4] ^ 0x5A5A5A5A])
+    hp = probes.cpu().numpy().view(np.uint32).astype(np.uint64)
+    pk, pv, pc = eng.route(probes, None, 4, 0, 0, 0, V, G)
+    pc = pc.cpu().tolist()
+    tot = np.zeros(2, np.int64)
+    start = 0
+    for g in range(G):
+        base, cnt = shard_range(V, G, g)
+        kk, vv = sk[sum(counts[:g]):sum(counts[:g + 1])], sv[sum(counts[:g]):sum(counts[:g + 1])]
+        t = eng.build(kk, vv, V, base, max(cnt, 1), BuildConfig(load_factor=load), 0)
+        tot += eng.probe_totals(t, pk[start:start + pc[g]]).cpu().numpy()
+        start += pc[g]
+    ro = oracle.probe_standard(ref, hp)
+    assert tot.tolist() == [ro["match_count"], ro["key_comparisons"]]
