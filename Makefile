@@ -10,7 +10,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
            --expt-relaxed-constexpr -Iinclude $(EXTRA_NVFLAGS)
 
-all: $(PKG)/libhg_b200.so oracle
+all: $(PKG)/libhg_b200.so oracle tests/cpp/test_dropin
 
 build/%.o: $(PKG)/csrc/%.cu $(HDR)
 	@mkdir -p build
@@ -30,3 +30,11 @@ clean:
 	$(MAKE) -s -f oracle/Makefile clean
 
 .PHONY: all oracle clean ptxas
+
+# C++ drop-in parity suite (runs on a GPU box; links the engine in-tree)
+tests/cpp/test_dropin: tests/cpp/test_dropin.cpp tests/cpp/mini_test.hpp include/hashgraph/*.hpp include/hg_b200.h $(PKG)/libhg_b200.so
+	g++ -std=c++20 -O2 -Wall -Wextra -Iinclude -o $@ tests/cpp/test_dropin.cpp \
+	  -L$(PKG) -lhg_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+
+cpptests: tests/cpp/test_dropin
+.PHONY: cpptests

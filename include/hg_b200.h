@@ -121,6 +121,14 @@ hg_status hg_table_device_arrays(const hg_table* t, const void** offsets, const 
 hg_status hg_table_export(const hg_table* t, uint64_t* offsets, uint64_t* keys, uint64_t* vals,
                           void* stream);
 
+/* A device table from caller arrays in the reference layout (HashGraph's
+ * constructor from offsets/edges, core.hpp:71-77): offsets[V+1], keys[N],
+ * vals[N] as u64 (host or device). No validation is done here; hg_validate
+ * checks the invariants. */
+hg_status hg_table_import(const uint64_t* offsets, const uint64_t* keys, const uint64_t* vals,
+                          uint64_t num_vertices, uint64_t num_edges, uint64_t hash_seed,
+                          double load_factor, int32_t hash_kind, void* stream, hg_table** out);
+
 /* Frees the table's device buffers in stream order. */
 hg_status hg_table_destroy(hg_table* t, void* stream);
 

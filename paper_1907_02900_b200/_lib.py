@@ -98,6 +98,8 @@ SIGNATURES = {
     "hg_table_device_arrays": (_i32, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)]),
     "hg_table_export": (_i32, [_vp, _vp, _vp, _vp, _vp]),
     "hg_table_destroy": (_i32, [_vp, _vp]),
+    "hg_table_import": (_i32, [_vp, _vp, _vp, _u64, _u64, _u64, C.c_double, _i32, _vp,
+                               C.POINTER(_vp)]),
     "hg_probe": (_i32, [_vp, _vp, _i32, _u64, C.POINTER(hg_probe_options),
                         C.POINTER(hg_probe_result), _vp]),
     "hg_count_instances": (_i32, [_vp, _u64, C.POINTER(_u64), _vp]),

@@ -282,6 +282,47 @@ hg_status hg_build(const void* keys, int32_t key_width, const void* vals, int32_
     return HG_OK;
 }
 
+hg_status hg_table_import(const uint64_t* offsets, const uint64_t* keys, const uint64_t* vals,
+                          uint64_t num_vertices, uint64_t num_edges, uint64_t hash_seed,
+                          double load_factor, int32_t hash_kind, void* stream, hg_table** out) {
+    if (!out) return fail(HG_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (num_vertices < 1) return fail(HG_EINVAL, "table has no vertices");
+    if (!offsets || (num_edges && (!keys || !vals))) return fail(HG_EINVAL, "NULL array");
+    if (hash_kind != HG_HASH_MIX64 && hash_kind != HG_HASH_IDENTITY)
+        return fail(HG_EINVAL, "unknown hash_kind");
+    int dev = 0;
+    if (hg_status st = need_device(&dev); st != HG_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto* t = new hg_table;
+    t->device = dev;
+    t->load_factor = load_factor;
+    hg::TableDesc& d = t->d;
+    d.nv = num_vertices;
+    d.n = num_edges;
+    d.seed = hash_seed;
+    d.hash_kind = hash_kind;
+    d.key_bytes = d.val_bytes = d.off_bytes = 8;
+    cudaError_t e = cudaMallocAsync(&t->alloc_offs, (num_vertices + 2) * 8, s);
+    if (e == cudaSuccess && num_edges) e = cudaMallocAsync(&d.keys, num_edges * 8, s);
+    if (e == cudaSuccess && num_edges) e = cudaMallocAsync(&d.vals, num_edges * 8, s);
+    if (e == cudaSuccess) {
+        d.offs = static_cast<char*>(t->alloc_offs) + 8;
+        e = cudaMemcpyAsync(d.offs, offsets, (num_vertices + 1) * 8, cudaMemcpyDefault, s);
+    }
+    if (e == cudaSuccess && num_edges)
+        e = cudaMemcpyAsync(d.keys, keys, num_edges * 8, cudaMemcpyDefault, s);
+    if (e == cudaSuccess && num_edges)
+        e = cudaMemcpyAsync(d.vals, vals, num_edges * 8, cudaMemcpyDefault, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        hg_table_destroy(t, stream);
+        return cuda_fail(e, "hg_table_import");
+    }
+    *out = t;
+    return HG_OK;
+}
+
 hg_status hg_table_get_info(const hg_table* t, hg_table_info* info) {
     if (!t || !info) return fail(HG_EINVAL, "NULL argument");
     info->num_vertices = t->d.nv;
