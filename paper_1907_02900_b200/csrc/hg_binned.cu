@@ -53,7 +53,7 @@ struct BuildLayout {
     static size_t bytes(uint32_t P) { return align16(size_t(P) * 4) + in_bytes() + k_bytes() + v_bytes(); }
 };
 
-template <typename K, typename VT, typename OffT, bool POW2>
+template <typename K, typename VT, typename OffT, int POW2>
 __global__ void __launch_bounds__(kBuildBlock)
 k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
              const OffT* __restrict__ part_start /* nparts + 1 partition offsets */,
@@ -153,14 +153,16 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
         }
         __syncthreads();
         // exclusive scan of cnt[0..pv): thread owns `per` consecutive counters
+        // (vectorised 16-byte shared loads/stores when per is a multiple of 4)
         const uint32_t per = (pv + kBuildBlock - 1) / kBuildBlock;
         const uint32_t j0 = min(pv, tid * per), j1 = min(pv, j0 + per);
+        const bool vec = (per & 3) == 0 && j1 - j0 == per && per <= 16;
         uint32_t run = 0;
-        const bool vec4 = per == 4 && j1 - j0 == 4;
-        uint4 c4 = make_uint4(0, 0, 0, 0);
-        if (vec4) {
-            c4 = lds128(cnt + j0);
-            run = c4.x + c4.y + c4.z + c4.w;
+        if (vec) {
+            for (uint32_t q = 0; q < per; q += 4) {
+                const uint4 c4 = lds128(cnt + j0 + q);
+                run += c4.x + c4.y + c4.z + c4.w;
+            }
         } else {
             for (uint32_t j = j0; j < j1; ++j) run += cnt[j];
         }
@@ -184,19 +186,25 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
         }
         __syncthreads();
         uint32_t acc = s_warp[warp] + inc - run;
-        if (vec4) {
-            const uint4 st = make_uint4(acc, acc + c4.x, acc + c4.x + c4.y, acc + c4.x + c4.y + c4.z);
-            sts128(cnt + j0, st);
-            if constexpr (sizeof(OffT) == 4) {
-                // offs + 1 is 16-byte aligned (hg_capi pads it) and vb + j0 is a multiple of 4
-                *reinterpret_cast<uint4*>(offs + vb + j0 + 1) =
-                    make_uint4(uint32_t(s) + st.y, uint32_t(s) + st.z, uint32_t(s) + st.w,
-                               uint32_t(s) + acc + run);
-            } else {
-                offs[vb + j0 + 1] = OffT(s + st.y);
-                offs[vb + j0 + 2] = OffT(s + st.z);
-                offs[vb + j0 + 3] = OffT(s + st.w);
-                offs[vb + j0 + 4] = OffT(s + acc + run);
+        if (vec) {
+            for (uint32_t q = 0; q < per; q += 4) {
+                const uint4 c4 = lds128(cnt + j0 + q);
+                const uint4 st = make_uint4(acc, acc + c4.x, acc + c4.x + c4.y,
+                                            acc + c4.x + c4.y + c4.z);
+                sts128(cnt + j0 + q, st);
+                const uint32_t nxt = st.w + c4.w;
+                if constexpr (sizeof(OffT) == 4) {
+                    // offs + 1 is 16-byte aligned (hg_capi pads it); vb + j0 + q is a multiple of 4
+                    *reinterpret_cast<uint4*>(offs + vb + j0 + q + 1) =
+                        make_uint4(uint32_t(s) + st.y, uint32_t(s) + st.z, uint32_t(s) + st.w,
+                                   uint32_t(s) + nxt);
+                } else {
+                    offs[vb + j0 + q + 1] = OffT(s + st.y);
+                    offs[vb + j0 + q + 2] = OffT(s + st.z);
+                    offs[vb + j0 + q + 3] = OffT(s + st.w);
+                    offs[vb + j0 + q + 4] = OffT(s + nxt);
+                }
+                acc = nxt;
             }
         } else {
             for (uint32_t j = j0; j < j1; ++j) {
@@ -241,7 +249,7 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
     if (tid == 0) bulk_wait_all();
 }
 
-template <typename K, typename VT, typename OffT, bool POW2>
+template <typename K, typename VT, typename OffT, int POW2>
 cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s) {
     using E = typename EntryT<K, VT>::T;
     const Divisor nv = make_divisor(global_nv(t), t.vbase);
@@ -295,11 +303,10 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
     return e;
 }
 
-#define HG_INST(K, VT, OffT)                                                                   \
-    template cudaError_t build_v2_impl<K, VT, OffT, true>(const TableDesc&, const BuildArgs&, \
-                                                          cudaStream_t);                       \
-    template cudaError_t build_v2_impl<K, VT, OffT, false>(const TableDesc&, const BuildArgs&, \
-                                                           cudaStream_t);
+#define HG_INST1(K, VT, OffT, HM) \
+    template cudaError_t build_v2_impl<K, VT, OffT, HM>(const TableDesc&, const BuildArgs&, cudaStream_t);
+#define HG_INST(K, VT, OffT) \
+    HG_INST1(K, VT, OffT, 0) HG_INST1(K, VT, OffT, 1) HG_INST1(K, VT, OffT, 2) HG_INST1(K, VT, OffT, 3)
 HG_INST(uint32_t, uint32_t, uint32_t)
 HG_INST(uint32_t, uint32_t, uint64_t)
 HG_INST(uint32_t, uint64_t, uint32_t)
@@ -308,6 +315,7 @@ HG_INST(uint64_t, uint32_t, uint32_t)
 HG_INST(uint64_t, uint32_t, uint64_t)
 HG_INST(uint64_t, uint64_t, uint32_t)
 HG_INST(uint64_t, uint64_t, uint64_t)
+#undef HG_INST1
 #undef HG_INST
 
 }  // namespace hg

@@ -83,14 +83,13 @@ __device__ __forceinline__ void for_each_key(const K* __restrict__ keys, uint64_
 
 // ---------------------------------------------------------------- K1 / K3
 
-template <typename K, typename OffT, bool POW2>
+template <typename K, typename OffT, int POW2>
 __global__ void __launch_bounds__(256)
 k_hash_count(const K* __restrict__ keys, uint64_t n, uint64_t seed, int hk, Divisor nv,
              OffT* __restrict__ cnt, int aggregate) {
     constexpr bool V32 = sizeof(OffT) == 4;
     for_each_key(keys, n, [&](uint64_t, K key) {
-        const uint64_t v = hk == kHashIdentity ? vertex_of<kHashIdentity, POW2>(key, seed, nv)
-                                               : vertex_of<kHashMix64, POW2>(key, seed, nv);
+        const uint64_t v = vhash<POW2>(key, seed, nv);
         if (aggregate) {
             aggregated_count<V32>(cnt + v, __activemask(), v);
         } else {
@@ -99,15 +98,14 @@ k_hash_count(const K* __restrict__ keys, uint64_t n, uint64_t seed, int hk, Divi
     });
 }
 
-template <typename K, typename VT, typename OffT, bool POW2>
+template <typename K, typename VT, typename OffT, int POW2>
 __global__ void __launch_bounds__(256)
 k_scatter(const K* __restrict__ keys, const VT* __restrict__ vals, uint64_t n, uint64_t seed,
           int hk, Divisor nv, OffT* __restrict__ cursor, K* __restrict__ okeys,
           VT* __restrict__ ovals, int aggregate) {
     constexpr bool V32 = sizeof(OffT) == 4;
     for_each_key(keys, n, [&](uint64_t i, K key) {
-        const uint64_t v = hk == kHashIdentity ? vertex_of<kHashIdentity, POW2>(key, seed, nv)
-                                               : vertex_of<kHashMix64, POW2>(key, seed, nv);
+        const uint64_t v = vhash<POW2>(key, seed, nv);
         OffT pos;
         if (aggregate) {
             pos = aggregated_ticket<V32>(cursor + v, __activemask(), v);
@@ -256,7 +254,7 @@ static cudaError_t stable_order(const TableDesc& t, cudaStream_t s) {
 
 // ------------------------------------------------------------------ V1
 
-template <typename K, typename VT, typename OffT, bool POW2>
+template <typename K, typename VT, typename OffT, int POW2>
 static cudaError_t build_v1_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s) {
     const Divisor nv = make_divisor(global_nv(t), t.vbase);
     OffT* offs = static_cast<OffT*>(t.offs);
@@ -280,21 +278,16 @@ static cudaError_t build_v1_impl(const TableDesc& t, const BuildArgs& a, cudaStr
 }
 
 // Binned build, hg_binned.cu.
-template <typename K, typename VT, typename OffT, bool POW2>
+template <typename K, typename VT, typename OffT, int POW2>
 cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s);
 
 template <typename K, typename VT, typename OffT>
 static cudaError_t build_typed(const TableDesc& t, const BuildArgs& a, cudaStream_t s) {
-    const uint64_t gv = global_nv(t);
-    const bool pow2 = (gv & (gv - 1)) == 0;
-    cudaError_t e;
-    if (a.variant == 2) {
-        e = pow2 ? build_v2_impl<K, VT, OffT, true>(t, a, s)
-                 : build_v2_impl<K, VT, OffT, false>(t, a, s);
-    } else {
-        e = pow2 ? build_v1_impl<K, VT, OffT, true>(t, a, s)
-                 : build_v1_impl<K, VT, OffT, false>(t, a, s);
-    }
+    cudaError_t e = dispatch_hash_mode(hash_mode(global_nv(t), t.hash_kind), [&](auto hm) {
+        constexpr int HM = decltype(hm)::value;
+        return a.variant == 2 ? build_v2_impl<K, VT, OffT, HM>(t, a, s)
+                              : build_v1_impl<K, VT, OffT, HM>(t, a, s);
+    });
     if (e == cudaSuccess && a.stable) e = stable_order<K, VT, OffT>(t, s);
     return e;
 }

@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace hg {
@@ -40,7 +41,7 @@ inline Divisor make_divisor(uint64_t d, uint64_t base = 0) {
     return r;
 }
 
-template <bool POW2>
+template <int POW2>
 __device__ __forceinline__ uint64_t mod_of(uint64_t h, const Divisor& m) {
     if constexpr (POW2) {
         return h & (m.d - 1);
@@ -51,7 +52,7 @@ __device__ __forceinline__ uint64_t mod_of(uint64_t h, const Divisor& m) {
     }
 }
 
-template <bool POW2>
+template <int POW2>
 __device__ __forceinline__ uint64_t div_of(uint64_t h, const Divisor& m) {
     if constexpr (POW2) {
         return h >> m.shift;
@@ -75,12 +76,35 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
 // hash.hpp:30-33; keys narrower than 64 bits are zero-extended first (the
 // reference API is u64-only, core.hpp:161). kHashIdentity restates the
 // fixture hasher of tests/support.hpp:42-46 (key % V).
-template <int HK, bool POW2>
+template <int HK, int POW2>
 __device__ __forceinline__ uint64_t vertex_of(uint64_t key, uint64_t seed, const Divisor& nv) {
     if constexpr (HK == kHashIdentity) {
         return mod_of<POW2>(key, nv) - nv.base;
     } else {
         return mod_of<POW2>(mix64(key ^ seed), nv) - nv.base;
+    }
+}
+
+// Hash mode HM (a template parameter of every kernel): bit 0 = V is a power
+// of two (mask instead of magic reduction), bit 1 = identity hasher.
+template <int HM>
+__device__ __forceinline__ uint64_t vhash(uint64_t key, uint64_t seed, const Divisor& nv) {
+    return vertex_of<(HM & 2) ? kHashIdentity : kHashMix64, (HM & 1) != 0>(key, seed, nv);
+}
+
+inline int hash_mode(uint64_t global_vertices, int hash_kind) {
+    return ((global_vertices & (global_vertices - 1)) == 0 ? 1 : 0) |
+           (hash_kind == kHashIdentity ? 2 : 0);
+}
+
+// Calls f(std::integral_constant<int, HM>{}) for the runtime hash mode.
+template <typename F>
+inline auto dispatch_hash_mode(int hm, F&& f) {
+    switch (hm) {
+        case 0: return f(std::integral_constant<int, 0>{});
+        case 1: return f(std::integral_constant<int, 1>{});
+        case 2: return f(std::integral_constant<int, 2>{});
+        default: return f(std::integral_constant<int, 3>{});
     }
 }
 

@@ -33,10 +33,9 @@ int num_sms();
 constexpr int kProbeBlock = 256;
 constexpr uint64_t kLongSeg = 32;
 
-template <bool POW2>
+template <int POW2>
 __device__ __forceinline__ uint64_t pvtx(uint64_t key, uint64_t seed, int hk, const Divisor& nv) {
-    return hk == kHashIdentity ? vertex_of<kHashIdentity, POW2>(key, seed, nv)
-                               : vertex_of<kHashMix64, POW2>(key, seed, nv);
+    return vhash<POW2>(key, seed, nv);
 }
 
 // Loads the VEC probes of this lane for warp chunk `base` (VEC*32 probes per
@@ -62,7 +61,7 @@ __device__ __forceinline__ void load_probes(const K* probes, uint64_t m, uint64_
     }
 }
 
-template <typename K, typename OffT, bool POW2, bool WRITE_COUNTS>
+template <typename K, typename OffT, int POW2, bool WRITE_COUNTS>
 __global__ void __launch_bounds__(kProbeBlock)
 k_probe_count(const K* __restrict__ probes, uint64_t m, uint64_t seed, int hk, Divisor nv,
               const OffT* __restrict__ offs, const K* __restrict__ tkeys,
@@ -154,7 +153,7 @@ __device__ __forceinline__ void store_pair(void* pairs, uint64_t slot, uint64_t 
     }
 }
 
-template <typename K, typename VT, typename OffT, typename PT, bool POW2>
+template <typename K, typename VT, typename OffT, typename PT, int POW2>
 __global__ void __launch_bounds__(kProbeBlock)
 k_probe_write(const K* __restrict__ probes, uint64_t m, uint64_t seed, int hk, Divisor nv,
               const OffT* __restrict__ offs, const K* __restrict__ tkeys,
@@ -238,7 +237,7 @@ struct ProbeLayout {
 // partition's offsets slice, its table-key slice and its probe entries into
 // shared memory (one mbarrier), then every probe is answered from shared
 // memory. Slices larger than the caps are read from global memory instead.
-template <typename K, typename VT, typename OffT, typename IT, bool POW2, int MODE, bool ORIG,
+template <typename K, typename VT, typename OffT, typename IT, int POW2, int MODE, bool ORIG,
           typename PT>
 __global__ void __launch_bounds__(kPartProbeBlock)
 k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __restrict__ ppart,
@@ -307,77 +306,86 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
         const uint64_t tb = s_tb;
         const uint64_t q0 = s_q0, qn = s_q1 - s_q0;
         const OffT* soff = reinterpret_cast<const OffT*>(b_off + s_o0);
-        const K* kp = s_kst ? reinterpret_cast<const K*>(b_key + s_o1) : tkeys + tb;
-        const PEnt* ep = s_pst ? reinterpret_cast<const PEnt*>(b_ent + s_o2) : pin + q0;
         mbar_wait(&s_bar, phase);
         phase ^= 1;
-        for (uint64_t base = uint64_t(warp) * 32; base < qn; base += uint64_t(nwarps) * 32) {
-            const uint64_t i = base + lane;
-            const bool valid = i < qn;
-            K key = 0;
-            typename std::conditional<std::is_void<IT>::value, uint32_t, IT>::type pidx = 0;
-            uint64_t b = 0, e = 0;
-            if (valid) {
-                const auto ent = ep[i];
-                key = PE::key(ent);
-                if constexpr (PE::kHasVal) pidx = PE::val(ent);
-                const uint32_t lv = uint32_t(hv<POW2>(key, seed, hk, nv) - vb);
-                b = uint64_t(soff[lv]) - tb;
-                e = uint64_t(soff[lv + 1]) - tb;
-            }
-            const uint64_t len = e - b;
-            compared += len;
-            uint32_t c = 0;
-            if (len <= kLongSeg)
-                for (uint64_t t = b; t < e; ++t) c += kp[t] == key;
-            uint32_t longm = __ballot_sync(0xffffffffu, len > kLongSeg);
-            while (longm) {
-                const int src = __ffs(longm) - 1;
-                longm &= longm - 1;
-                const uint64_t kb = __shfl_sync(0xffffffffu, b, src);
-                const uint64_t ke = __shfl_sync(0xffffffffu, e, src);
-                const K kk = __shfl_sync(0xffffffffu, key, src);
-                uint32_t cc = 0;
-                for (uint64_t t = kb + lane; t < ke; t += 32) cc += kp[t] == kk;
-                cc = warp_sum(cc);
-                if (int(lane) == src) c = cc;
-            }
-            matches += c;
-            if constexpr (MODE == 1) {
+        // Probe loop, instantiated for the common case (slices staged in
+        // shared memory: LDS on 32-bit addresses) and for oversized slices
+        // (generic loads from global memory).
+        auto run = [&](const K* __restrict__ kp, const PEnt* __restrict__ ep) {
+            for (uint64_t base = uint64_t(warp) * 32; base < qn; base += uint64_t(nwarps) * 32) {
+                const uint64_t i = base + lane;
+                const bool valid = i < qn;
+                K key = 0;
+                typename std::conditional<std::is_void<IT>::value, uint32_t, IT>::type pidx = 0;
+                uint64_t b = 0, e = 0;
                 if (valid) {
-                    if constexpr (ORIG) pcount[pidx] = c;
-                    else pcount[q0 + i] = c;
+                    const auto ent = ep[i];
+                    key = PE::key(ent);
+                    if constexpr (PE::kHasVal) pidx = PE::val(ent);
+                    const uint32_t lv = uint32_t(hv<POW2>(key, seed, hk, nv) - vb);
+                    b = uint64_t(soff[lv]) - tb;
+                    e = uint64_t(soff[lv + 1]) - tb;
                 }
-            }
-            if constexpr (MODE == 2) {
-                uint64_t sl = (valid && c) ? pair_off[q0 + i] : 0;
-                if (valid && c && len <= kLongSeg) {
-                    for (uint64_t t = b; t < e && sl < cap; ++t) {
-                        if (kp[t] == key) {
-                            store_pair<PT>(pairs, sl, uint64_t(tvals[tb + t]), uint64_t(pidx));
-                            ++sl;
-                        }
-                    }
-                }
-                uint32_t lm = __ballot_sync(0xffffffffu, valid && c && len > kLongSeg);
-                while (lm) {
-                    const int src = __ffs(lm) - 1;
-                    lm &= lm - 1;
+                const uint64_t len = e - b;
+                compared += len;
+                uint32_t c = 0;
+                if (len <= kLongSeg)
+                    for (uint64_t t = b; t < e; ++t) c += kp[t] == key;
+                uint32_t longm = __ballot_sync(0xffffffffu, len > kLongSeg);
+                while (longm) {
+                    const int src = __ffs(longm) - 1;
+                    longm &= longm - 1;
                     const uint64_t kb = __shfl_sync(0xffffffffu, b, src);
                     const uint64_t ke = __shfl_sync(0xffffffffu, e, src);
                     const K kk = __shfl_sync(0xffffffffu, key, src);
-                    uint64_t ws = __shfl_sync(0xffffffffu, sl, src);
-                    const uint64_t pj = __shfl_sync(0xffffffffu, uint64_t(pidx), src);
-                    for (uint64_t t0 = kb; t0 < ke && ws < cap; t0 += 32) {
-                        const uint64_t t = t0 + lane;
-                        const bool hit = t < ke && kp[t] == kk;
-                        const uint32_t hm = __ballot_sync(0xffffffffu, hit);
-                        const uint64_t my = ws + __popc(hm & lanemask_lt());
-                        if (hit && my < cap) store_pair<PT>(pairs, my, uint64_t(tvals[tb + t]), pj);
-                        ws += __popc(hm);
+                    uint32_t cc = 0;
+                    for (uint64_t t = kb + lane; t < ke; t += 32) cc += kp[t] == kk;
+                    cc = warp_sum(cc);
+                    if (int(lane) == src) c = cc;
+                }
+                matches += c;
+                if constexpr (MODE == 1) {
+                    if (valid) {
+                        if constexpr (ORIG) pcount[pidx] = c;
+                        else pcount[q0 + i] = c;
+                    }
+                }
+                if constexpr (MODE == 2) {
+                    uint64_t sl = (valid && c) ? pair_off[q0 + i] : 0;
+                    if (valid && c && len <= kLongSeg) {
+                        for (uint64_t t = b; t < e && sl < cap; ++t) {
+                            if (kp[t] == key) {
+                                store_pair<PT>(pairs, sl, uint64_t(tvals[tb + t]), uint64_t(pidx));
+                                ++sl;
+                            }
+                        }
+                    }
+                    uint32_t lm = __ballot_sync(0xffffffffu, valid && c && len > kLongSeg);
+                    while (lm) {
+                        const int src = __ffs(lm) - 1;
+                        lm &= lm - 1;
+                        const uint64_t kb = __shfl_sync(0xffffffffu, b, src);
+                        const uint64_t ke = __shfl_sync(0xffffffffu, e, src);
+                        const K kk = __shfl_sync(0xffffffffu, key, src);
+                        uint64_t ws = __shfl_sync(0xffffffffu, sl, src);
+                        const uint64_t pj = __shfl_sync(0xffffffffu, uint64_t(pidx), src);
+                        for (uint64_t t0 = kb; t0 < ke && ws < cap; t0 += 32) {
+                            const uint64_t t = t0 + lane;
+                            const bool hit = t < ke && kp[t] == kk;
+                            const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+                            const uint64_t my = ws + __popc(hm & lanemask_lt());
+                            if (hit && my < cap) store_pair<PT>(pairs, my, uint64_t(tvals[tb + t]), pj);
+                            ws += __popc(hm);
+                        }
                     }
                 }
             }
+        };
+        if (s_kst && s_pst) {
+            run(reinterpret_cast<const K*>(b_key + s_o1), reinterpret_cast<const PEnt*>(b_ent + s_o2));
+        } else {
+            run(s_kst ? reinterpret_cast<const K*>(b_key + s_o1) : tkeys + tb,
+                s_pst ? reinterpret_cast<const PEnt*>(b_ent + s_o2) : pin + q0);
         }
         __syncthreads();
     }
@@ -409,7 +417,7 @@ __global__ void k_scatter_counts(const typename EntryT<K, IT>::T* __restrict__ p
         counts[EntryT<K, IT>::val(pin[i])] = pcount[i];
 }
 
-template <typename K, typename VT, typename OffT, typename IT, bool POW2>
+template <typename K, typename VT, typename OffT, typename IT, int POW2>
 static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cudaStream_t s) {
     const Divisor nv = make_divisor(global_nv(t), t.vbase);
     const OffT* offs = static_cast<const OffT*>(t.offs);
@@ -540,7 +548,7 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
     return e;
 }
 
-template <typename K, typename VT, typename OffT, bool POW2>
+template <typename K, typename VT, typename OffT, int POW2>
 static cudaError_t probe_impl(const TableDesc& t, const ProbeArgs& a, cudaStream_t s) {
     const Divisor nv = make_divisor(global_nv(t), t.vbase);
     const OffT* offs = static_cast<const OffT*>(t.offs);
@@ -608,9 +616,9 @@ static cudaError_t probe_impl(const TableDesc& t, const ProbeArgs& a, cudaStream
 
 template <typename K, typename VT, typename OffT>
 static cudaError_t probe_pow(const TableDesc& t, const ProbeArgs& a, cudaStream_t s) {
-    const uint64_t gv = global_nv(t);
-    return (gv & (gv - 1)) == 0 ? probe_impl<K, VT, OffT, true>(t, a, s)
-                                    : probe_impl<K, VT, OffT, false>(t, a, s);
+    return dispatch_hash_mode(hash_mode(global_nv(t), t.hash_kind), [&](auto hm) {
+        return probe_impl<K, VT, OffT, decltype(hm)::value>(t, a, s);
+    });
 }
 template <typename K, typename VT>
 static cudaError_t probe_off(const TableDesc& t, const ProbeArgs& a, cudaStream_t s) {

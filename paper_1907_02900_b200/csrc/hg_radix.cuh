@@ -63,10 +63,9 @@ struct EntryT<K, void> {
     __device__ static uint32_t val(const T&) { return 0; }
 };
 
-template <bool POW2>
+template <int POW2>
 __device__ __forceinline__ uint64_t hv(uint64_t key, uint64_t seed, int hk, const Divisor& nv) {
-    return hk == kHashIdentity ? vertex_of<kHashIdentity, POW2>(key, seed, nv)
-                               : vertex_of<kHashMix64, POW2>(key, seed, nv);
+    return vhash<POW2>(key, seed, nv);
 }
 
 // ------------------------------------------------------------ geometry
@@ -112,7 +111,7 @@ inline PartGeom make_geom(uint64_t nv, uint64_t n, uint64_t want_pv, double targ
 
 constexpr int kHistBlock = 1024;
 
-template <typename K, typename OffT, bool POW2>
+template <typename K, typename OffT, int POW2>
 __global__ void __launch_bounds__(kHistBlock)
 k_part_hist(const K* __restrict__ keys, uint64_t n, uint64_t seed, int hk, Divisor nv,
             uint32_t pshift, uint32_t nparts, OffT* __restrict__ hist) {
@@ -197,7 +196,7 @@ struct SplitLayout {
     static constexpr size_t kBytes = kSplitStages * kInBytes + size_t(kTile) * (sizeof(E) + 1);
 };
 
-template <typename K, typename VT, typename OffT, bool RAW, bool PASS2, bool POW2>
+template <typename K, typename VT, typename OffT, bool RAW, bool PASS2, int POW2>
 __global__ void __launch_bounds__(kSplitBlock)
 k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t n, uint64_t seed,
              int hk, Divisor nv, uint32_t pshift, uint32_t dshift, uint32_t dmask, uint32_t b2,
@@ -397,7 +396,7 @@ struct PartitionScratch {
 // out[part_start[p] .. part_start[p+1]) holds the entries of partition p
 // (p = h(key) >> pshift). part_start (nparts + 1 entries, device) receives
 // the partition offsets; part_start[nparts] = n.
-template <typename K, typename VT, typename OffT, bool POW2>
+template <typename K, typename VT, typename OffT, int POW2>
 cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, int hk,
                       const Divisor& nv, const PartGeom& g, OffT* part_start, void* scratch,
                       typename EntryT<K, VT>::T* out, cudaStream_t s, const char* tag) {

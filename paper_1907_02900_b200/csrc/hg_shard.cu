@@ -24,15 +24,14 @@ constexpr int kRouteBlock = 512;
 constexpr int kRouteItems = 4;
 constexpr int kRouteTile = kRouteBlock * kRouteItems;
 
-template <bool POW2>
+template <int POW2>
 __device__ __forceinline__ uint32_t owner_of(uint64_t key, uint64_t seed, int hk, const Divisor& gv,
                                              const Divisor& span) {
-    const uint64_t v = hk == kHashIdentity ? vertex_of<kHashIdentity, POW2>(key, seed, gv)
-                                           : vertex_of<kHashMix64, POW2>(key, seed, gv);
+    const uint64_t v = vhash<POW2>(key, seed, gv);
     return uint32_t(div_of<false>(v, span));
 }
 
-template <typename K, bool POW2>
+template <typename K, int POW2>
 __global__ void __launch_bounds__(kRouteBlock)
 k_route_hist(const K* __restrict__ keys, uint64_t n, uint64_t seed, int hk, Divisor gv,
              Divisor span, uint32_t shards, unsigned long long* __restrict__ counts) {
@@ -47,7 +46,7 @@ k_route_hist(const K* __restrict__ keys, uint64_t n, uint64_t seed, int hk, Divi
         if (sh[i]) atomicAdd(counts + i, (unsigned long long)sh[i]);
 }
 
-template <typename K, typename VT, bool POW2>
+template <typename K, typename VT, int POW2>
 __global__ void __launch_bounds__(kRouteBlock)
 k_route_scatter(const K* __restrict__ keys, const VT* __restrict__ vals, uint64_t n,
                 uint64_t val_base, uint64_t seed, int hk, Divisor gv, Divisor span,
@@ -108,7 +107,7 @@ k_route_scatter(const K* __restrict__ keys, const VT* __restrict__ vals, uint64_
     }
 }
 
-template <typename K, typename VT, bool POW2>
+template <typename K, typename VT, int POW2>
 static cudaError_t route_typed(const void* keys, const void* vals, uint64_t n, uint64_t val_base,
                                uint64_t seed, int hk, uint64_t V, uint32_t G, void* out_keys,
                                void* out_vals, uint64_t* shard_counts, cudaStream_t s) {
@@ -149,14 +148,13 @@ cudaError_t route_keys(const void* keys, int key_bytes, const void* vals, int va
                        uint64_t n, uint64_t val_base, uint64_t seed, int hash_kind,
                        uint64_t global_vertices, uint32_t shards, void* out_keys, void* out_vals,
                        uint64_t* shard_counts, cudaStream_t s) {
-    const bool pow2 = (global_vertices & (global_vertices - 1)) == 0;
+    const int hm = hash_mode(global_vertices, hash_kind);
 #define HG_ROUTE(K, VT)                                                                        \
-    return pow2 ? route_typed<K, VT, true>(keys, vals, n, val_base, seed, hash_kind,           \
-                                           global_vertices, shards, out_keys, out_vals,        \
-                                           shard_counts, s)                                    \
-                : route_typed<K, VT, false>(keys, vals, n, val_base, seed, hash_kind,          \
-                                            global_vertices, shards, out_keys, out_vals,       \
-                                            shard_counts, s)
+    return dispatch_hash_mode(hm, [&](auto m) {                                                \
+        return route_typed<K, VT, decltype(m)::value>(keys, vals, n, val_base, seed, hash_kind, \
+                                                      global_vertices, shards, out_keys,       \
+                                                      out_vals, shard_counts, s);              \
+    })
     if (key_bytes == 4) {
         if (val_bytes == 4) HG_ROUTE(uint32_t, uint32_t);
         HG_ROUTE(uint32_t, uint64_t);

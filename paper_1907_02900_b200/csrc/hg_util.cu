@@ -81,7 +81,7 @@ cudaError_t generate_keys(void* out, int key_bytes, uint64_t n, int kind, uint64
 // its key does not hash to, 8 index out of range, 9 duplicate index,
 // 10 key != input[index]. The smallest code found wins (atomicMin).
 
-template <typename K, typename VT, typename OffT, bool POW2>
+template <typename K, typename VT, typename OffT, int POW2>
 __global__ void k_validate_vertices(const OffT* __restrict__ offs, uint64_t nv, uint64_t n,
                                     uint64_t seed, int hk, Divisor dv, const K* __restrict__ keys,
                                     uint32_t* code) {
@@ -99,8 +99,7 @@ __global__ void k_validate_vertices(const OffT* __restrict__ offs, uint64_t nv, 
         }
         if (e > n) continue;  // reported via code 4/5
         for (uint64_t j = b; j < e; ++j) {
-            const uint64_t h = hk == kHashIdentity ? vertex_of<kHashIdentity, POW2>(keys[j], seed, dv)
-                                                   : vertex_of<kHashMix64, POW2>(keys[j], seed, dv);
+            const uint64_t h = vhash<POW2>(keys[j], seed, dv);
             if (h != v) {
                 atomicMin(code, 7u);
                 break;
@@ -133,15 +132,12 @@ static cudaError_t validate_typed(const TableDesc& t, const void* input, uint32_
     if (e != cudaSuccess) return e;
     const Divisor dv = make_divisor(global_nv(t), t.vbase);
     const unsigned grid = unsigned(num_sms()) * 8;
-    if ((global_nv(t) & (global_nv(t) - 1)) == 0) {
-        k_validate_vertices<K, VT, OffT, true><<<grid, 256, 0, s>>>(
+    dispatch_hash_mode(hash_mode(global_nv(t), t.hash_kind), [&](auto hm) {
+        k_validate_vertices<K, VT, OffT, decltype(hm)::value><<<grid, 256, 0, s>>>(
             static_cast<const OffT*>(t.offs), t.nv, t.n, t.seed, t.hash_kind, dv,
             static_cast<const K*>(t.keys), d_code);
-    } else {
-        k_validate_vertices<K, VT, OffT, false><<<grid, 256, 0, s>>>(
-            static_cast<const OffT*>(t.offs), t.nv, t.n, t.seed, t.hash_kind, dv,
-            static_cast<const K*>(t.keys), d_code);
-    }
+        return 0;
+    });
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (t.n) {
         void* seen = nullptr;
