@@ -114,21 +114,43 @@ class ClockSampler:
 
 
 def alg_bytes(name: str, n: int, v: int, m: int, c: int, kb: int = 4, vb: int = 4,
-              ob: int = 4) -> int:
-    """Algorithmic bytes of one launch at array granularity (SURVEY.md 8(d)
-    convention: each pass reads each input array once and writes each output
-    once; an atomically updated array counts read + write). DESIGN.md lists
-    the same table."""
+              ob: int = 4, probe_ent: int = 4) -> int:
+    """Algorithmic bytes of ONE launch of kernel `name`:
+    compulsory traffic at array granularity -- each pass reads each input
+    array once and writes each output array once. n build keys, v vertices,
+    m probes, c key comparisons; kb/vb/ob key/value/offset widths; probe_ent
+    = bytes of a partitioned probe entry (4: key only for count-only probes)."""
+    e = kb + vb  # build entry (key, value)
     return {
+        # simple build (V1)
         "k1_hash_count": n * kb + 2 * v * ob,
         "k2_scan": 2 * v * ob,
-        "k3_scatter": n * kb + 2 * v * ob + n * (kb + vb),
+        "k3_scatter": n * kb + 2 * v * ob + n * e,
+        # binned build (V2)
         "k4_part_hist": n * kb,
-        "k5_part_scan": 0,
-        "k6_part_scatter": n * kb + n * (kb + vb),
-        "k7_part_build": 2 * n * (kb + vb) + v * ob,
+        "k6a_multisplit": n * kb + n * e,
+        "k6b_multisplit": 2 * n * e,
+        "k7_part_build": n * e + n * e + v * ob,
+        # partitioned probe
+        "p4_part_hist": m * kb,
+        "p6a_multisplit": m * kb + m * probe_ent,
+        "p6b_multisplit": 2 * m * probe_ent,
+        "k8p_probe_part": m * probe_ent + (v + 1) * ob + n * kb,
+        # direct probe
         "k8_probe_count": m * kb + (v + 1) * ob + c * kb,
     }.get(name, 0)
+
+
+def reference_alg_bytes(variant: int, n: int, v: int, m: int, c: int, kb: int = 4, vb: int = 4,
+                        ob: int = 4, sc: int = 4, bins: int = 1 << 15) -> int:
+    """SURVEY.md 8(d) reference-loop-nest bytes of one step (build + count-only
+    probe): V1 = N(3sk+sv) + V(7sc+2so) + so, V2 = N(6sk+3sv) + (V+B)(7sc+2so)
+    + 2so, probe = M sk + (V+1) so + C sk + M sc."""
+    if variant == 1:
+        build = n * (3 * kb + vb) + v * (7 * sc + 2 * ob) + ob
+    else:
+        build = n * (6 * kb + 3 * vb) + (v + bins) * (7 * sc + 2 * ob) + 2 * ob
+    return build + m * kb + (v + 1) * ob + c * kb + m * sc
 
 
 # ------------------------------------------------------------------ reference arm
@@ -283,13 +305,17 @@ def run_b200(args):
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(dom)
+        traffic = json.load(open(tpath)).get("kernels", {}).get(dom)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                 "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                 "alg_bytes_per_launch": ab, "avg_launch_ms": round(avg_ms, 4),
                 "peak_source": peak_src,
                 "step_alg_bytes": sum(alg_bytes(k, local_n, local_v, local_m, comparisons) * kern[k][0]
                                       for k in kern) // max(1, args.steps)}
+    ref_bytes = reference_alg_bytes(args.variant, local_n, local_v, local_m,
+                                    comparisons if world == 1 else int(engine.last_local_c))
+    roofline["step_reference_alg_bytes"] = ref_bytes
+    roofline["step_reference_frac"] = round(ref_bytes / (ms * 1e-3) / 1e9 / peak, 4)
     kernels = {k: {"launches": l, "avg_ms": round(t / l, 4), "share": round(t / sum(
         x[1] for x in kern.values()), 4)} for k, (l, t) in sorted(kern.items(), key=lambda x: -x[1][1])}
 

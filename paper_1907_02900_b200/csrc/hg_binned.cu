@@ -41,6 +41,7 @@ namespace hg {
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 constexpr int kBuildBlock = 512;
+static const char* const kBuildPassNames[3] = {"k4_part_hist", "k6a_multisplit", "k6b_multisplit"};
 
 template <typename K, typename VT>
 struct BuildLayout {
@@ -282,7 +283,7 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
         if ((e = cudaMemsetAsync(ticket, 0, 4, s)) != cudaSuccess) break;
         e = partition<K, VT, OffT, POW2>(static_cast<const K*>(a.keys),
                                          static_cast<const VT*>(a.vals), t.n, t.seed, t.hash_kind,
-                                         nv, g, part_start, pscratch, reorg, s, "k4_part_hist");
+                                         nv, g, part_start, pscratch, reorg, s, kBuildPassNames);
         if (e != cudaSuccess) break;
         auto kb = k_part_build<K, VT, OffT, POW2>;
         if ((e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -218,6 +218,7 @@ k_probe_write(const K* __restrict__ probes, uint64_t m, uint64_t seed, int hk, D
 // ------------------------------------------------------------ partitioned
 
 constexpr int kPartProbeBlock = 512;
+static const char* const kProbePassNames[3] = {"p4_part_hist", "p6a_multisplit", "p6b_multisplit"};
 
 // Shared memory per CTA: offsets slice (P+1) | table keys slice (kcap) |
 // probe entries of the partition (pcap), all filled by TMA bulk copies.
@@ -469,11 +470,11 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
         if (need_idx) {
             e = partition<K, IT, OffT, POW2>(probes, static_cast<const IT*>(nullptr), a.m, t.seed,
                                              t.hash_kind, nv, g, ppart, pscratch,
-                                             static_cast<E1*>(reorg), s, "p_part_hist");
+                                             static_cast<E1*>(reorg), s, kProbePassNames);
         } else {
             e = partition<K, void, OffT, POW2>(probes, static_cast<const void*>(nullptr), a.m,
                                                t.seed, t.hash_kind, nv, g, ppart, pscratch,
-                                               static_cast<E0*>(reorg), s, "p_part_hist");
+                                               static_cast<E0*>(reorg), s, kProbePassNames);
         }
         if (e != cudaSuccess) break;
         const size_t smem = ProbeLayout<K, OffT, E1>::bytes(P, kcap, pcap);

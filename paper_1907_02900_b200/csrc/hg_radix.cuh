@@ -399,7 +399,7 @@ struct PartitionScratch {
 template <typename K, typename VT, typename OffT, int POW2>
 cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, int hk,
                       const Divisor& nv, const PartGeom& g, OffT* part_start, void* scratch,
-                      typename EntryT<K, VT>::T* out, cudaStream_t s, const char* tag) {
+                      typename EntryT<K, VT>::T* out, cudaStream_t s, const char* const names[3]) {
     using PS = PartitionScratch<K, VT, OffT>;
     using E = typename EntryT<K, VT>::T;
     char* p = static_cast<char*>(scratch);
@@ -429,7 +429,7 @@ cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, 
     unsigned grid = unsigned(std::max(1, per_sm) * sms);
     grid = unsigned(std::max<uint64_t>(
         1, std::min<uint64_t>(grid, (n + kHistBlock * 16 - 1) / (kHistBlock * 16))));
-    HG_LAUNCH(tag, s, kh<<<grid, kHistBlock, hsmem, s>>>(keys, n, seed, hk, nv, g.pshift,
+    HG_LAUNCH(names[0], s, kh<<<grid, kHistBlock, hsmem, s>>>(keys, n, seed, hk, nv, g.pshift,
                                                         uint32_t(g.nparts), hist));
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = launch_scan<OffT, OffT>(hist, part_start, g.nparts, scan_scr, part_start + g.nparts, s,
@@ -459,20 +459,20 @@ cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, 
         1, std::min<uint64_t>(tiles1 + 1, uint64_t(sms) * std::max(1, occ2))));
     if (g.b2 == 0) {
         // single pass straight into partition order
-        HG_LAUNCH("multisplit1", s,
+        HG_LAUNCH(names[1], s,
                   (ks1<<<g1, kSplitBlock, sm1, s>>>(
                       keys, vals, n, seed, hk, nv, g.pshift, 0, uint32_t((1u << g.b1) - 1), 0,
                       cur2, part_start, 0, nullptr, tiles1, g.nparts, out)));
         return cudaGetLastError();
     }
-    HG_LAUNCH("multisplit1", s,
+    HG_LAUNCH(names[1], s,
               (ks1<<<g1, kSplitBlock, sm1, s>>>(
                   keys, vals, n, seed, hk, nv, g.pshift, g.b2, uint32_t((1u << g.b1) - 1), 0, cur1,
                   part_start, 0, nullptr, tiles1, g.nparts, mid)));
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     k_tile_prefix<OffT><<<1, 32, 0, s>>>(part_start, g.nparts, nb1, g.b2, kSplitTile, tile_prefix);
     const uint64_t tiles2 = tiles1 + nb1;  // upper bound; exact count = tile_prefix[nb1]
-    HG_LAUNCH("multisplit2", s,
+    HG_LAUNCH(names[2], s,
               (ks2<<<g2, kSplitBlock, sm2, s>>>(
                   mid, nullptr, n, seed, hk, nv, g.pshift, 0, uint32_t((1u << g.b2) - 1), g.b2,
                   cur2, part_start, nb1, tile_prefix, tiles2, g.nparts, out)));
