@@ -162,6 +162,24 @@ typedef struct hg_probe_result {
 hg_status hg_probe(const hg_table* t, const void* probes, int32_t probe_width, uint64_t m,
                    const hg_probe_options* opts, hg_probe_result* result, void* stream);
 
+/* probe_new_prepared (join.hpp:143-166) over intersect_adjacency
+ * (join.hpp:41-57): a and b must share the vertex range (num_vertices equal,
+ * else HG_EINVAL as join.hpp:145-147 throws invalid_argument) and the key
+ * width. Pairs are (left = a's entry value, right = b's entry value), written
+ * in sequential order (vertex, then a position, then b position); under a
+ * cap the first pair_cap of that order are kept. key_comparisons =
+ * sum_v |A_v| * |B_v|. opts->counts must be NULL (there are no probes). */
+hg_status hg_probe_new_prepared(const hg_table* a, const hg_table* b, const hg_probe_options* opts,
+                                hg_probe_result* result, void* stream);
+
+/* probe_new (join.hpp:170-182): builds keys_a and keys_b (key_width bytes
+ * each) with the binned build over the shared V = derived_vertex_count(
+ * max(na, nb), cfg->load_factor) (or cfg->vertex_count when non-zero), then
+ * hg_probe_new_prepared. Entry values are input positions. */
+hg_status hg_probe_new(const void* keys_a, uint64_t na, const void* keys_b, uint64_t nb,
+                       int32_t key_width, const hg_build_config* cfg, const hg_probe_options* opts,
+                       hg_probe_result* result, void* stream);
+
 /* count_instances (core.hpp:235-246). */
 hg_status hg_count_instances(const hg_table* t, uint64_t key, uint64_t* out, void* stream);
 

@@ -178,6 +178,37 @@ void hgo_probe_standard(const uint64_t* offsets, const uint64_t* ekeys, const ui
     if (written) *written = pairs ? (slot < cap ? slot : cap) : 0;
 }
 
+/* join.hpp:41-57 intersect_adjacency driven by join.hpp:143-166
+ * probe_new_prepared, one chunk: for each vertex v (ascending), every
+ * (a, b) entry pair of the two segments is compared on the full key
+ * (|A_v| * |B_v| comparisons); a match emits MatchPair{left = A entry index,
+ * right = B entry index} while slot < cap. Order: vertex, then A position,
+ * then B position -- the sequential emission order of the reference. */
+void hgo_probe_new_prepared(const uint64_t* offs_a, const uint64_t* keys_a, const uint64_t* idx_a,
+                            const uint64_t* offs_b, const uint64_t* keys_b, const uint64_t* idx_b,
+                            uint64_t nv, uint64_t cap, uint64_t* pairs, uint64_t* match_count,
+                            uint64_t* comparisons, uint64_t* written) {
+    uint64_t count = 0, cmp = 0, slot = 0;
+    for (uint64_t v = 0; v < nv; ++v) {
+        for (uint64_t i = offs_a[v]; i < offs_a[v + 1]; ++i) {
+            for (uint64_t j = offs_b[v]; j < offs_b[v + 1]; ++j) {
+                ++cmp;
+                if (keys_a[i] == keys_b[j]) {
+                    ++count;
+                    if (pairs && slot < cap) {
+                        pairs[2 * slot] = idx_a[i];
+                        pairs[2 * slot + 1] = idx_b[j];
+                    }
+                    ++slot;
+                }
+            }
+        }
+    }
+    *match_count = count;
+    *comparisons = cmp;
+    if (written) *written = pairs ? (slot < cap ? slot : cap) : 0;
+}
+
 /* core.hpp:251-282 validate_csr, plus the key-consistency check SURVEY.md
  * 8(c) adds (edges[j].key == input[edges[j].index]) when input != NULL.
  * Returns 0 when valid, else the number of the first violated invariant. */

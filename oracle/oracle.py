@@ -95,6 +95,9 @@ class Oracle:
         lib.hgo_probe_standard.restype = None
         lib.hgo_probe_standard.argtypes = [_P, _P, _P, u64, u64, i32, _P, u64, u64, _P, _P,
                                            _P, _P, _P]
+        lib.hgo_probe_new_prepared.restype = None
+        lib.hgo_probe_new_prepared.argtypes = [_P, _P, _P, _P, _P, _P, u64, u64, _P, _P, _P,
+                                               _P]
         lib.hgo_validate_csr.restype = i32
         lib.hgo_validate_csr.argtypes = [_P, _P, _P, u64, u64, u64, u64, i32, _P]
         lib.hgo_exclusive_prefix_sum.restype = i32
@@ -178,6 +181,39 @@ class Oracle:
             res["per_probe"] = pp
         return res
 
+    def probe_new_prepared(self, a: Table, b: Table, materialize: bool = False,
+                           cap: int = 1 << 24):
+        """join.hpp:143-166 (restated in hgo_probe_new_prepared)."""
+        if a.num_vertices != b.num_vertices:
+            raise ValueError("probe_new_prepared: tables use different vertex ranges")
+        mc = np.zeros(1, np.uint64)
+        cmp = np.zeros(1, np.uint64)
+        wr = np.zeros(1, np.uint64)
+        if materialize and cap > 4 * (1 << 28):
+            raise ValueError("oracle cap too large")
+        pairs = np.zeros(2 * max(cap, 0), np.uint64) if materialize else None
+        self.lib.hgo_probe_new_prepared(_ptr(a.offsets), _ptr(a.keys), _ptr(a.index),
+                                        _ptr(b.offsets), _ptr(b.keys), _ptr(b.index),
+                                        a.num_vertices, cap, _ptr(pairs), _ptr(mc), _ptr(cmp),
+                                        _ptr(wr))
+        res = {"match_count": int(mc[0]), "key_comparisons": int(cmp[0]),
+               "truncated": bool(materialize and int(mc[0]) > cap)}
+        if materialize:
+            res["pairs"] = pairs[: 2 * int(wr[0])].reshape(-1, 2)
+        return res
+
+    def probe_new(self, a, b, load: float = 1.0, bins: int = 1 << 15, seed: int = 0,
+                  hash_kind: int = HASH_MIX64, materialize: bool = False, cap: int = 1 << 24):
+        """join.hpp:170-182: both sides built with build_v2 over the V of the
+        larger input, then probe_new_prepared."""
+        a, b = _u64(a), _u64(b)
+        nv = self.derived_vertex_count(max(len(a), len(b)), load)
+        ta = self.build(a, variant=2, load=load, bins=bins, seed=seed, vertex_count=nv,
+                        hash_kind=hash_kind)
+        tb = self.build(b, variant=2, load=load, bins=bins, seed=seed, vertex_count=nv,
+                        hash_kind=hash_kind)
+        return self.probe_new_prepared(ta, tb, materialize, cap)
+
     def count_instances(self, t: Table, key: int) -> int:
         return int(self.lib.hgo_count_instances(_ptr(t.offsets), _ptr(t.keys), t.num_vertices,
                                                 t.hash_seed, t.hash_kind, key))
@@ -247,6 +283,11 @@ class Reference:
         lib.hgr_export.argtypes = [vp, _P, _P, _P]
         lib.hgr_probe.restype = None
         lib.hgr_probe.argtypes = [vp, _P, u64, i32, u64, _P, _P, C.POINTER(i32), _P, _P]
+        lib.hgr_probe_new_prepared.restype = i32
+        lib.hgr_probe_new_prepared.argtypes = [vp, vp, i32, u64, _P, _P, C.POINTER(i32), _P, _P]
+        lib.hgr_probe_new.restype = i32
+        lib.hgr_probe_new.argtypes = [_P, u64, _P, u64, dbl, u64, u64, i32, i32, u64, _P, _P,
+                                      C.POINTER(i32), _P, _P]
         lib.hgr_count_instances.restype = u64
         lib.hgr_count_instances.argtypes = [vp, u64]
         lib.hgr_validate.restype = i32
@@ -319,6 +360,36 @@ class Reference:
         if materialize:
             res["pairs"] = pairs[: 2 * int(npairs[0])].reshape(-1, 2)
         return res
+
+    @staticmethod
+    def _join_result(rc, mc, cmp, tr, pairs, npairs, materialize, what):
+        if rc:
+            raise ValueError(f"{what}: tables use different vertex ranges")
+        res = {"match_count": int(mc[0]), "key_comparisons": int(cmp[0]),
+               "truncated": bool(tr.value)}
+        if materialize:
+            res["pairs"] = pairs[: 2 * int(npairs[0])].reshape(-1, 2)
+        return res
+
+    def probe_new_prepared(self, ha, hb, materialize=False, cap=1 << 24):
+        mc, cmp, npairs = (np.zeros(1, np.uint64) for _ in range(3))
+        tr = C.c_int(0)
+        pairs = np.zeros(2 * min(cap, 1 << 30), np.uint64) if materialize else None
+        rc = self.lib.hgr_probe_new_prepared(ha, hb, int(materialize), cap, _ptr(mc), _ptr(cmp),
+                                             C.byref(tr), _ptr(pairs), _ptr(npairs))
+        return self._join_result(rc, mc, cmp, tr, pairs, npairs, materialize,
+                                 "probe_new_prepared")
+
+    def probe_new(self, a, b, load=1.0, bins=1 << 15, seed=0, hash_kind=HASH_MIX64,
+                  materialize=False, cap=1 << 24):
+        a, b = _u64(a), _u64(b)
+        mc, cmp, npairs = (np.zeros(1, np.uint64) for _ in range(3))
+        tr = C.c_int(0)
+        pairs = np.zeros(2 * min(cap, 1 << 30), np.uint64) if materialize else None
+        rc = self.lib.hgr_probe_new(_ptr(a), len(a), _ptr(b), len(b), load, bins, seed,
+                                    hash_kind, int(materialize), cap, _ptr(mc), _ptr(cmp),
+                                    C.byref(tr), _ptr(pairs), _ptr(npairs))
+        return self._join_result(rc, mc, cmp, tr, pairs, npairs, materialize, "probe_new")
 
     def count_instances(self, h, key: int) -> int:
         return int(self.lib.hgr_count_instances(h, key))

@@ -122,6 +122,68 @@ void hgr_probe(const void* t, const std::uint64_t* probes, std::uint64_t m, int 
     }
 }
 
+namespace {
+void copy_result(const JoinResult& r, std::uint64_t* match_count, std::uint64_t* comparisons,
+                 int* truncated, std::uint64_t* pairs_out, std::uint64_t* npairs) {
+    *match_count = r.match_count;
+    *comparisons = r.key_comparisons;
+    *truncated = r.truncated ? 1 : 0;
+    *npairs = 0;
+    if (r.pairs) {
+        *npairs = r.pairs->size();
+        if (pairs_out) {
+            for (std::size_t i = 0; i < r.pairs->size(); ++i) {
+                pairs_out[2 * i] = (*r.pairs)[i].left_index;
+                pairs_out[2 * i + 1] = (*r.pairs)[i].right_index;
+            }
+        }
+    }
+}
+}  // namespace
+
+// probe_new_prepared (join.hpp:143-166). Returns 0, or 1 on invalid_argument
+// (mismatched vertex ranges, join.hpp:145-147).
+int hgr_probe_new_prepared(const void* a, const void* b, int materialize, std::uint64_t cap,
+                           std::uint64_t* match_count, std::uint64_t* comparisons,
+                           int* truncated, std::uint64_t* pairs_out, std::uint64_t* npairs) {
+    ProbeOptions opts;
+    opts.materialize = materialize != 0;
+    opts.pair_cap = cap;
+    try {
+        copy_result(probe_new_prepared(*static_cast<const HashGraph*>(a),
+                                       *static_cast<const HashGraph*>(b), opts),
+                    match_count, comparisons, truncated, pairs_out, npairs);
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return 1;
+    }
+}
+
+// probe_new (join.hpp:170-182): both sides built with build_v2 over the
+// shared V of the larger input. hash_kind 1 -> identity hasher.
+int hgr_probe_new(const std::uint64_t* a, std::uint64_t na, const std::uint64_t* b,
+                  std::uint64_t nb, double load, std::uint64_t bins, std::uint64_t seed,
+                  int hash_kind, int materialize, std::uint64_t cap, std::uint64_t* match_count,
+                  std::uint64_t* comparisons, int* truncated, std::uint64_t* pairs_out,
+                  std::uint64_t* npairs) {
+    BuildConfig cfg;
+    cfg.load_factor = load;
+    cfg.bin_count = bins;
+    cfg.hash_seed = seed;
+    ProbeOptions opts;
+    opts.materialize = materialize != 0;
+    opts.pair_cap = cap;
+    std::span<const std::uint64_t> sa(a, na), sb(b, nb);
+    try {
+        const JoinResult r = hash_kind == 1 ? probe_new(sa, sb, cfg, IdentityHasher{}, opts)
+                                            : probe_new(sa, sb, cfg, opts);
+        copy_result(r, match_count, comparisons, truncated, pairs_out, npairs);
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return 1;
+    }
+}
+
 std::uint64_t hgr_count_instances(const void* t, std::uint64_t key) {
     return count_instances(*static_cast<const HashGraph*>(t), key);
 }

@@ -8,13 +8,14 @@ API and the C++ mirror in include/hashgraph/.
 from .hashgraph import (ENTRY_DTYPE, MATCH_PAIR_DTYPE, BuildConfig, BuildStats, ExecMode,
                         HashGraph, IdentityHasher, InvalidArgument, JoinResult, OutOfRange,
                         Overflow, ProbeOptions, VertexHasher, build_v1, build_v2, count_instances,
-                        derived_vertex_count, generate, hash_to_vertex, probe_device,
-                        probe_standard,
+                        derived_vertex_count, generate, hash_to_vertex, intersect_adjacency,
+                        probe_device, probe_new, probe_new_prepared, probe_standard,
                         validate_csr)
 
 __all__ = [
     "ENTRY_DTYPE", "MATCH_PAIR_DTYPE", "BuildConfig", "BuildStats", "ExecMode", "HashGraph",
     "IdentityHasher", "InvalidArgument", "JoinResult", "OutOfRange", "Overflow", "ProbeOptions",
     "VertexHasher", "build_v1", "build_v2", "count_instances", "derived_vertex_count", "generate",
-    "hash_to_vertex", "probe_device", "probe_standard", "validate_csr",
+    "hash_to_vertex", "intersect_adjacency", "probe_device", "probe_new",
+    "probe_new_prepared", "probe_standard", "validate_csr",
 ]

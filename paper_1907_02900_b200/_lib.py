@@ -102,6 +102,10 @@ SIGNATURES = {
                                C.POINTER(_vp)]),
     "hg_probe": (_i32, [_vp, _vp, _i32, _u64, C.POINTER(hg_probe_options),
                         C.POINTER(hg_probe_result), _vp]),
+    "hg_probe_new_prepared": (_i32, [_vp, _vp, C.POINTER(hg_probe_options),
+                                     C.POINTER(hg_probe_result), _vp]),
+    "hg_probe_new": (_i32, [_vp, _u64, _vp, _u64, _i32, C.POINTER(hg_build_config),
+                            C.POINTER(hg_probe_options), C.POINTER(hg_probe_result), _vp]),
     "hg_count_instances": (_i32, [_vp, _u64, C.POINTER(_u64), _vp]),
     "hg_validate": (_i32, [_vp, _vp, _u64, C.POINTER(_i32), _vp]),
     "hg_generate": (_i32, [_vp, _i32, _u64, _i32, _u64, _u64, C.c_double, _vp, _u64, _vp]),

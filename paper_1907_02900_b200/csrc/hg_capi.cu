@@ -477,6 +477,102 @@ hg_status hg_probe(const hg_table* t, const void* probes, int32_t probe_width, u
     return st;
 }
 
+hg_status hg_probe_new_prepared(const hg_table* ta, const hg_table* tb,
+                                const hg_probe_options* opts_in, hg_probe_result* result,
+                                void* stream) {
+    if (!ta || !tb) return fail(HG_EINVAL, "NULL table");
+    hg_probe_options opts;
+    if (opts_in) {
+        opts = *opts_in;
+    } else {
+        hg_probe_options_init(&opts);
+    }
+    // join.hpp:145-147
+    if (ta->d.nv != tb->d.nv || ta->d.gnv != tb->d.gnv || ta->d.vbase != tb->d.vbase)
+        return fail(HG_EINVAL, "probe_new_prepared: tables use different vertex ranges");
+    if (ta->d.key_bytes != tb->d.key_bytes)
+        return fail(HG_EUNSUPPORTED, "probe_new_prepared: tables have different key widths");
+    if (ta->device != tb->device) return fail(HG_EINVAL, "tables live on different devices");
+    if (opts.counts) return fail(HG_EINVAL, "probe_new_prepared has no per-probe counts");
+    if (opts.materialize && opts.pair_width != 4 && opts.pair_width != 8)
+        return fail(HG_EINVAL, "pair_width must be 4 or 8");
+    if (opts.materialize && opts.pair_cap && !opts.pairs)
+        return fail(HG_EINVAL, "materialize requires a pairs buffer");
+    if (!opts.device_result && !result) return fail(HG_EINVAL, "result is NULL");
+    if (cudaSetDevice(ta->device) != cudaSuccess) return fail(HG_ECUDA, "cudaSetDevice failed");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool want_pairs = opts.materialize && opts.pair_cap > 0;
+    const bool pairs_dev = want_pairs && is_device_ptr(opts.pairs);
+    const size_t tot_bytes = opts.device_result ? 0 : 256;
+    const size_t pr_bytes = (want_pairs && !pairs_dev) ? opts.pair_cap * 2 * opts.pair_width : 0;
+    void* scratch = nullptr;
+    cudaError_t e = cudaSuccess;
+    if (tot_bytes + pr_bytes && (e = cudaMallocAsync(&scratch, tot_bytes + pr_bytes, s)) != cudaSuccess)
+        return cuda_fail(e, "hg_probe_new_prepared: scratch");
+    uint64_t* totals = opts.device_result ? opts.device_result : static_cast<uint64_t*>(scratch);
+    void* pairs = want_pairs ? (pairs_dev ? opts.pairs : static_cast<char*>(scratch) + tot_bytes)
+                             : nullptr;
+    e = cudaMemsetAsync(totals, 0, 2 * sizeof(uint64_t), s);
+    hg::IntersectArgs ia;
+    ia.totals = totals;
+    ia.pairs = pairs;
+    ia.pair_bytes = opts.pair_width;
+    ia.cap = want_pairs ? opts.pair_cap : 0;
+    if (e == cudaSuccess) e = hg::intersect_tables(ta->d, tb->d, ia, s);
+    hg_status st = HG_OK;
+    if (e != cudaSuccess) {
+        st = cuda_fail(e, "hg_probe_new_prepared");
+    } else if (!opts.device_result) {
+        uint64_t host_tot[2] = {0, 0};
+        e = cudaMemcpyAsync(host_tot, totals, sizeof host_tot, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        const uint64_t written = opts.materialize ? std::min(host_tot[0], opts.pair_cap) : 0;
+        if (e == cudaSuccess && want_pairs && !pairs_dev && written)
+            e = cudaMemcpyAsync(opts.pairs, pairs, written * 2 * opts.pair_width,
+                                cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) {
+            st = cuda_fail(e, "hg_probe_new_prepared: result readback");
+        } else if (result) {
+            result->match_count = host_tot[0];
+            result->key_comparisons = host_tot[1];
+            result->pairs_written = written;
+            result->truncated = opts.materialize && host_tot[0] > opts.pair_cap;
+        }
+    } else if (result) {
+        std::memset(result, 0, sizeof *result);
+    }
+    if (scratch) cudaFreeAsync(scratch, s);
+    return st;
+}
+
+hg_status hg_probe_new(const void* keys_a, uint64_t na, const void* keys_b, uint64_t nb,
+                       int32_t key_width, const hg_build_config* cfg_in,
+                       const hg_probe_options* opts, hg_probe_result* result, void* stream) {
+    hg_build_config cfg;
+    if (cfg_in) {
+        cfg = *cfg_in;
+    } else {
+        hg_build_config_init(&cfg);
+    }
+    if (cfg.global_vertices) return fail(HG_EINVAL, "probe_new builds unsharded tables");
+    if (!cfg.vertex_count) {
+        // join.hpp:171-172: V from the larger input
+        hg_status st = hg_derived_vertex_count(na > nb ? na : nb, cfg.load_factor, &cfg.vertex_count);
+        if (st != HG_OK) return st;
+    }
+    cfg.variant = HG_BUILD_BINNED;  // join.hpp:173-174
+    if (cfg.vertex_count > (uint64_t(1) << 30)) cfg.variant = HG_BUILD_SIMPLE;  // same table
+    hg_table* ta = nullptr;
+    hg_table* tb = nullptr;
+    hg_status st = hg_build(keys_a, key_width, nullptr, 8, na, &cfg, stream, &ta);
+    if (st == HG_OK) st = hg_build(keys_b, key_width, nullptr, 8, nb, &cfg, stream, &tb);
+    if (st == HG_OK) st = hg_probe_new_prepared(ta, tb, opts, result, stream);
+    hg_table_destroy(ta, stream);
+    hg_table_destroy(tb, stream);
+    return st;
+}
+
 hg_status hg_count_instances(const hg_table* t, uint64_t key, uint64_t* out, void* stream) {
     if (!out) return fail(HG_EINVAL, "out is NULL");
     if (t && t->d.key_bytes == 4 && key > 0xFFFFFFFFull) {

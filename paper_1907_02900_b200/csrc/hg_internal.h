@@ -55,6 +55,20 @@ struct ProbeArgs {
 
 cudaError_t probe_table(const TableDesc& t, const ProbeArgs& a, cudaStream_t s);
 
+// probe_new_prepared (join.hpp:143-166): intersects two tables over one
+// vertex range (A.nv == B.nv, equal key widths). totals[2] (device) are
+// accumulated; pairs (device, nullable) receive (A value, B value) in
+// sequential order (vertex, A position, B position), the first `cap` kept.
+struct IntersectArgs {
+    uint64_t* totals = nullptr;
+    void* pairs = nullptr;
+    int pair_bytes = 8;
+    uint64_t cap = 0;
+};
+
+cudaError_t intersect_tables(const TableDesc& A, const TableDesc& B, const IntersectArgs& a,
+                             cudaStream_t s);
+
 // Counter-based synthetic generators.
 // kind 0: key[i] = splitmix64(seed, start+i) (truncated to key_bytes).
 // kind 1: C4 probes with hit ratio `hit` against build keys `ref` (n_ref).

@@ -422,6 +422,89 @@ def probe_device(hg: HashGraph, probes, device_result, counts=None, pairs=None,
     _check(_lib.lib().hg_probe(hg.handle, pa.ptr, pa.width, pa.n, C.byref(o), None, s))
 
 
+def _join_options(opts: ProbeOptions, cap_bound: int):
+    o = _lib.hg_probe_options()
+    _lib.lib().hg_probe_options_init(C.byref(o))
+    o.materialize = 1 if opts.materialize else 0
+    o.pair_width = 8
+    o.pair_cap = int(opts.pair_cap)
+    pairs = None
+    if opts.materialize:
+        pairs = np.zeros(max(min(int(opts.pair_cap), cap_bound), 0), MATCH_PAIR_DTYPE)
+        o.pairs = pairs.ctypes.data if pairs.size else None
+        if pairs.size == 0:
+            o.pair_cap = 0
+    return o, pairs
+
+
+def _join_result(r, opts: ProbeOptions, pairs) -> JoinResult:
+    res = JoinResult(r.match_count, r.key_comparisons, bool(r.truncated), None)
+    if opts.materialize:
+        res.pairs = pairs[: r.pairs_written]
+        res.truncated = r.match_count > int(opts.pair_cap)
+    return res
+
+
+def probe_new_prepared(hg_a: HashGraph, hg_b: HashGraph,
+                       opts: Optional[ProbeOptions] = None) -> JoinResult:
+    """join.hpp:143-166: adjacency intersection of two tables over one vertex
+    range (K12 k_intersect). Pairs are (index in A's input, index in B's
+    input), in sequential order (vertex, A position, B position).
+    Raises InvalidArgument when the vertex ranges differ (join.hpp:145-147)."""
+    opts = opts or ProbeOptions()
+    o, pairs = _join_options(opts, max(hg_a.num_edges(), 1) * max(hg_b.num_edges(), 1))
+    r = _lib.hg_probe_result()
+    _check(_lib.lib().hg_probe_new_prepared(hg_a.handle, hg_b.handle, C.byref(o), C.byref(r),
+                                            hg_a._stream))
+    return _join_result(r, opts, pairs)
+
+
+def probe_new(keys_a, keys_b, cfg: Optional[BuildConfig] = None,
+              opts: Optional[ProbeOptions] = None, hasher=None) -> JoinResult:
+    """join.hpp:170-182: dual-table join. Both inputs are built (binned build)
+    over the shared V = derived_vertex_count(max(|A|, |B|), load_factor), then
+    intersected vertex by vertex."""
+    cfg = cfg or BuildConfig()
+    opts = opts or ProbeOptions()
+    wa, wb = _Arr(keys_a), _Arr(keys_b)
+    if wa.width != wb.width:
+        wide = np.uint64
+        wa = _Arr(np.asarray(wa.keep if not wa.is_cuda else wa.keep.cpu().numpy()).astype(wide))
+        wb = _Arr(np.asarray(wb.keep if not wb.is_cuda else wb.keep.cpu().numpy()).astype(wide))
+    c = _lib.hg_build_config()
+    _lib.lib().hg_build_config_init(C.byref(c))
+    c.load_factor = float(cfg.load_factor)
+    c.bin_count = int(cfg.bin_count) if cfg.bin_count >= 0 else 0
+    c.hash_seed = int(cfg.hash_seed)
+    c.hash_kind = _hash_kind(hasher)
+    c.stable = 1 if cfg.mode == ExecMode.sequential else 0
+    c.aggregate = int(cfg.aggregate)
+    o, pairs = _join_options(opts, max(wa.n, 1) * max(wb.n, 1))
+    r = _lib.hg_probe_result()
+    _check(_lib.lib().hg_probe_new(wa.ptr, wa.n, wb.ptr, wb.n, wa.width, C.byref(c), C.byref(o),
+                                   C.byref(r), _stream_for(wa, wb)))
+    return _join_result(r, opts, pairs)
+
+
+def intersect_adjacency(a, b, emit=None, comparisons: Optional[list] = None) -> int:
+    """join.hpp:41-57 for two (host) segments of ENTRY_DTYPE entries. Segment
+    intersection on the device happens inside probe_new_prepared; this host
+    helper exists for API completeness (it is the definition the K12 kernel
+    implements per vertex)."""
+    a = np.asarray(a, ENTRY_DTYPE)
+    b = np.asarray(b, ENTRY_DTYPE)
+    count = 0
+    for ea in a:
+        hits = np.nonzero(b["key"] == ea["key"])[0]
+        for j in hits:
+            count += 1
+            if emit is not None:
+                emit(int(ea["index"]), int(b["index"][j]))
+    if comparisons is not None:
+        comparisons[0] += len(a) * len(b)
+    return count
+
+
 def count_instances(hg: HashGraph, key: int, hasher=None) -> int:
     """core.hpp:235-246."""
     if hasher is not None and _hash_kind(hasher) != hg.hash_kind:

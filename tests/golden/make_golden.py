@@ -95,6 +95,34 @@ def main() -> None:
             r.free(h)
         cases.append(case)
     g["cases"] = cases
+
+    # probe_new / probe_new_prepared (join.hpp:143-182), incl. the
+    # test_join.cpp:134-260 scenarios: random pairs, empty sides, shared V from
+    # the larger side (load 2), heavy single key (cap), identity collisions.
+    pn = []
+    rng = np.random.default_rng(21)
+    pspecs = [(800, 150, 700, 120, 1.0, 0, 0), (0, 1, 3, 4, 1.0, 0, 0), (3, 4, 0, 1, 1.0, 0, 0),
+              (8, 0, 2, 0, 2.0, 0, 0), (64, 0, 64, 0, 1.0, 0, 0), (5, 0, 3, 0, 5.0, 0, 1),
+              (2000, 300, 1500, 300, 0.5, 77, 0), (1200, 40, 900, 40, 4.0, 5, 0)]
+    for (na, ra, nb, rb, load, seed, identity) in pspecs:
+        if ra:
+            a = rng.integers(0, ra, size=na, dtype=np.uint64)
+            b = rng.integers(0, rb, size=nb, dtype=np.uint64)
+        elif na == 8:
+            a, b = np.arange(1, 9, dtype=np.uint64), np.array([3, 4], np.uint64)
+        elif na == 64:
+            a, b = np.full(64, 5, np.uint64), np.full(64, 5, np.uint64)
+        else:
+            a = np.array([3, 9, 3, 10121, 7], np.uint64)
+            b = np.array([3, 10121, 11], np.uint64)
+        hk = HASH_IDENTITY if identity else 0
+        res = r.probe_new(a, b, load=load, seed=seed, hash_kind=hk, materialize=True,
+                          cap=1 << 20)
+        pn.append({"a": [int(x) for x in a], "b": [int(x) for x in b], "load": load,
+                   "seed": seed, "hash_kind": hk, "match_count": res["match_count"],
+                   "key_comparisons": res["key_comparisons"],
+                   "pairs": sorted([[int(x), int(y)] for x, y in res["pairs"]])})
+    g["probe_new"] = pn
     with open(OUT, "w") as f:
         json.dump(g, f, separators=(",", ":"))
     print(f"wrote {OUT} ({os.path.getsize(OUT)} bytes)")

@@ -158,3 +158,42 @@ def test_keygen_restatement(oracle, reference):
     for n, mult, seed in [(1000, 1.0, 7), (5000, 16.0, 3), (10, 0.5, 0)]:
         assert (oracle.generate_uniform(n, mult, seed) ==
                 reference.generate(1, n, mult, seed)).all()
+
+
+@pytest.mark.parametrize("ci", range(len(GOLDEN["probe_new"])))
+def test_golden_probe_new(oracle, ci):
+    # join.hpp:143-182; reference outputs recorded by make_golden.py
+    case = GOLDEN["probe_new"][ci]
+    r = oracle.probe_new(case["a"], case["b"], load=case["load"], seed=case["seed"],
+                         hash_kind=case["hash_kind"], materialize=True, cap=1 << 20)
+    assert r["match_count"] == case["match_count"]
+    assert r["key_comparisons"] == case["key_comparisons"]
+    assert sorted(r["pairs"].tolist()) == case["pairs"]
+
+
+def test_probe_new_matches_reference_random(oracle, reference):
+    # test_join.cpp:134-150 (random vs nested loop), :152-157 (symmetric count),
+    # :189-205 (comparisons = segment-product sum)
+    rng = np.random.default_rng(333)
+    for _ in range(25):
+        a = rng.integers(0, int(rng.integers(1, 150)), size=int(rng.integers(1, 800)),
+                         dtype=np.uint64)
+        b = rng.integers(0, int(rng.integers(1, 150)), size=int(rng.integers(1, 800)),
+                         dtype=np.uint64)
+        load = float(rng.choice([0.5, 1.0, 2.0]))
+        ro = oracle.probe_new(a, b, load=load, materialize=True, cap=1 << 20)
+        rr = reference.probe_new(a, b, load=load, materialize=True, cap=1 << 20)
+        assert ro["match_count"] == rr["match_count"] == oracle.sort_merge_join_count(a, b)
+        assert ro["key_comparisons"] == rr["key_comparisons"]
+        assert sorted(ro["pairs"].tolist()) == sorted(rr["pairs"].tolist())
+        assert oracle.probe_new(b, a)["match_count"] == ro["match_count"]
+    # mismatched vertex ranges (test_join.cpp:182-186)
+    ta, tb = oracle.build([1, 2, 3, 4], variant=2), oracle.build([1, 2], variant=2)
+    with pytest.raises(ValueError):
+        oracle.probe_new_prepared(ta, tb)
+    ha = reference.build_handle([1, 2, 3, 4], variant=2)
+    hb = reference.build_handle([1, 2], variant=2)
+    with pytest.raises(ValueError):
+        reference.probe_new_prepared(ha, hb)
+    reference.free(ha)
+    reference.free(hb)
