@@ -359,6 +359,33 @@ def run_b200(args):
                                  "build_gkeys_s": round(n / (tb / reps * 1e-3) / 1e9, 3),
                                  "probe_ms": round(tp / reps, 4),
                                  "probe_gkeys_s": round(m / (tp / reps * 1e-3) / 1e9, 3)}
+        # probe_new (join.hpp:170-182): second table over the probes with the
+        # shared V, then the K12 intersect (count only)
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        tb = ti = 0.0
+        reps = 3
+        ta = hg.build_v2(keys, stream=sp)
+        for _ in range(reps):
+            e0.record(stream)
+            tbl_b = hg.build_v2(probes, vertex_count=nv, stream=sp)
+            e1.record(stream)
+            hg.probe_new_device(ta, tbl_b, result, stream=sp)
+            e2.record(stream)
+            tbl_b.close(sp)
+            torch.cuda.synchronize()
+            tb += e0.elapsed_time(e1)
+            ti += e1.elapsed_time(e2)
+        ta.close(sp)
+        pn_matches, pn_cmp = (int(x) for x in result.cpu().tolist())
+        ib = (nv + 1) * 4 * 2 + (n + m) * 4  # offsets of both tables + both key arrays
+        extras["probe_new"] = {
+            "build_b_ms": round(tb / reps, 4), "intersect_ms": round(ti / reps, 4),
+            "intersect_gkeys_s": round((n + m) / (ti / reps * 1e-3) / 1e9, 3),
+            "intersect_alg_gbs": round(ib / (ti / reps * 1e-3) / 1e9, 1),
+            "join_gkeys_s": round((n + m) / ((tb / reps + extras["v2"]["build_ms"] + ti / reps)
+                                             * 1e-3) / 1e9, 3),
+            "match_count": pn_matches, "key_comparisons": pn_cmp,
+            "matches_equal_probe_standard": pn_matches == matches}
         line["phases"] = extras
 
     # ---- e2e through the public API with pinned HOST buffers

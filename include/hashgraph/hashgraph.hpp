@@ -10,7 +10,8 @@
 //   core.hpp:21-26 Entry, :28 ExecMode, :30-35 BuildConfig, :40-56 BuildStats,
 //   :59-63 derived_vertex_count, :67-102 HashGraph, :160-177 build_v1,
 //   :183-230 build_v2, :235-246 count_instances, :251-287 validate_csr
-//   join.hpp:18-35 MatchPair / ProbeOptions / JoinResult, :110-136 probe_standard
+//   join.hpp:18-35 MatchPair / ProbeOptions / JoinResult, :110-136 probe_standard,
+//   :41-57 intersect_adjacency, :143-166 probe_new_prepared, :170-182 probe_new
 //
 // Differences, by construction of a device engine:
 //   * hashers: VertexHasher and hashgraph::IdentityHasher (key % V) run on
@@ -446,6 +447,97 @@ JoinResult probe_standard(const HashGraph& hg, std::span<const std::uint64_t> pr
 inline JoinResult probe_standard(const HashGraph& hg, std::span<const std::uint64_t> probe_keys,
                                  const ProbeOptions& opts = {}) {
     return probe_standard(hg, probe_keys, VertexHasher{hg.hash_seed()}, opts);
+}
+
+// join.hpp:41-57. Host helper over two segments (spans of Entry, e.g. from
+// HashGraph::vertex_entries). The device engine never calls it: the
+// per-vertex intersection runs inside probe_new_prepared (K12 k_intersect).
+template <class Emit>
+std::uint64_t intersect_adjacency(std::span<const Entry> a, std::span<const Entry> b, Emit&& emit,
+                                  std::uint64_t* comparisons = nullptr) {
+    std::uint64_t count = 0;
+    for (const Entry& ea : a)
+        for (const Entry& eb : b)
+            if (ea.key == eb.key) {
+                ++count;
+                emit(ea.index, eb.index);
+            }
+    if (comparisons) *comparisons += std::uint64_t(a.size()) * b.size();
+    return count;
+}
+
+namespace detail {
+inline JoinResult join_result(const hg_probe_result& r, const ProbeOptions& opts,
+                              std::vector<MatchPair>&& pairs) {
+    JoinResult res;
+    res.match_count = r.match_count;
+    res.key_comparisons = r.key_comparisons;
+    if (opts.materialize) {
+        pairs.resize(r.pairs_written);
+        res.truncated = r.match_count > opts.pair_cap;
+        res.pairs = std::move(pairs);
+    }
+    return res;
+}
+
+inline hg_probe_options join_options(const ProbeOptions& opts, std::uint64_t bound,
+                                     std::vector<MatchPair>& pairs) {
+    hg_probe_options o;
+    hg_probe_options_init(&o);
+    o.materialize = opts.materialize ? 1 : 0;
+    o.pair_width = 8;
+    o.pair_cap = opts.pair_cap;
+    if (opts.materialize) {
+        pairs.resize(std::min<std::uint64_t>(opts.pair_cap, bound));
+        o.pairs = pairs.data();
+        if (pairs.empty()) o.pair_cap = 0;
+    }
+    return o;
+}
+}  // namespace detail
+
+// join.hpp:143-166. Throws std::invalid_argument when the tables use
+// different vertex ranges (join.hpp:145-147). Pairs are (index in A's input,
+// index in B's input) in sequential order (vertex, A position, B position).
+inline JoinResult probe_new_prepared(const HashGraph& hg_a, const HashGraph& hg_b,
+                                     const ProbeOptions& opts = {}) {
+    std::vector<MatchPair> pairs;
+    const hg_probe_options o = detail::join_options(
+        opts, std::max<std::uint64_t>(hg_a.num_edges(), 1) * std::max<std::uint64_t>(hg_b.num_edges(), 1),
+        pairs);
+    hg_probe_result r{};
+    detail::check(hg_probe_new_prepared(hg_a.device_table(), hg_b.device_table(), &o, &r, nullptr));
+    return detail::join_result(r, opts, std::move(pairs));
+}
+
+// join.hpp:170-182: both inputs built (binned build) over the V of the
+// larger input, then intersected vertex by vertex.
+template <VertexHashFn H>
+JoinResult probe_new(std::span<const std::uint64_t> keys_a, std::span<const std::uint64_t> keys_b,
+                     const BuildConfig& cfg, const H& hasher, const ProbeOptions& opts = {}) {
+    static_assert(device_hasher<H>::supported, "hasher has no device implementation");
+    detail::check_config(cfg);
+    hg_build_config c;
+    hg_build_config_init(&c);
+    c.load_factor = cfg.load_factor;
+    c.bin_count = cfg.bin_count;
+    c.hash_seed = device_hasher<H>::seed(hasher);
+    c.hash_kind = device_hasher<H>::kind;
+    c.stable = cfg.mode == ExecMode::sequential ? 1 : 0;
+    std::vector<MatchPair> pairs;
+    const hg_probe_options o = detail::join_options(
+        opts, std::max<std::uint64_t>(keys_a.size(), 1) * std::max<std::uint64_t>(keys_b.size(), 1),
+        pairs);
+    hg_probe_result r{};
+    detail::check(hg_probe_new(keys_a.data(), keys_a.size(), keys_b.data(), keys_b.size(), 8, &c,
+                               &o, &r, nullptr));
+    return detail::join_result(r, opts, std::move(pairs));
+}
+
+inline JoinResult probe_new(std::span<const std::uint64_t> keys_a,
+                            std::span<const std::uint64_t> keys_b, const BuildConfig& cfg = {},
+                            const ProbeOptions& opts = {}) {
+    return probe_new(keys_a, keys_b, cfg, VertexHasher{cfg.hash_seed}, opts);
 }
 
 }  // namespace hashgraph

@@ -459,6 +459,23 @@ def probe_new_prepared(hg_a: HashGraph, hg_b: HashGraph,
     return _join_result(r, opts, pairs)
 
 
+def probe_new_device(hg_a: HashGraph, hg_b: HashGraph, device_result, pairs=None,
+                     pair_width: int = 4, pair_cap: int = 0, stream=None) -> None:
+    """Fully asynchronous probe_new_prepared on device-resident tables:
+    {match_count, key_comparisons} land in `device_result` (CUDA u64[2])."""
+    ra = _Arr(device_result)
+    o = _lib.hg_probe_options()
+    _lib.lib().hg_probe_options_init(C.byref(o))
+    o.device_result = ra.ptr
+    if pairs is not None:
+        o.materialize = 1
+        o.pair_width = pair_width
+        o.pair_cap = pair_cap
+        o.pairs = _Arr(pairs).ptr
+    s = stream if stream is not None else _stream_for(ra)
+    _check(_lib.lib().hg_probe_new_prepared(hg_a.handle, hg_b.handle, C.byref(o), None, s))
+
+
 def probe_new(keys_a, keys_b, cfg: Optional[BuildConfig] = None,
               opts: Optional[ProbeOptions] = None, hasher=None) -> JoinResult:
     """join.hpp:170-182: dual-table join. Both inputs are built (binned build)
