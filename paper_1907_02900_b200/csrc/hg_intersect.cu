@@ -7,13 +7,16 @@
 // both CSRs are walked in vertex order, i.e. the kernel is a streaming merge
 // of offsA, offsB, keysA, keysB (HBM-bound, every byte read once).
 //
-//   K12 k_intersect   persistent CTAs take vertex tiles (T = 2048 vertices)
-//                     from an atomic ticket; thread 0 stages the tile's two
-//                     offset slices and two key slices into shared memory
-//                     with TMA bulk copies (one mbarrier); each thread owns
-//                     T/256 consecutive vertices and compares every (a, b)
-//                     pair of a short segment pair serially; segment pairs
-//                     with |A_v|*|B_v| > kShortWork are flattened and strided
+//   K12 k_intersect   warp-specialised persistent CTAs. A producer warp takes
+//                     vertex tiles (T = 2048) from an atomic ticket and issues
+//                     TMA bulk copies of the tile's two offset slices and two
+//                     key slices into a 2-stage shared-memory ring (full /
+//                     empty mbarriers); 16 consumer warps intersect one tile
+//                     while the next is in flight. Consumer thread t owns
+//                     the tile vertices j*512 + t (conflict-free offset reads).
+//                     A segment pair with both sides <= kShort entries is
+//                     compared in registers (B side preloaded, predicated);
+//                     longer pairs are flattened (p = i*|B_v| + q) and strided
 //                     over the warp (skewed keys do not serialise one lane).
 //   pairs mode        the tile's match count is published with a decoupled
 //                     look-back (status words as in hg_scan.cuh), so the
@@ -25,6 +28,7 @@
 //                     subset; ours is the sequential one).
 // key_comparisons = sum_v |A_v|*|B_v| (join.hpp:52, test_join.cpp:189-205).
 #include <algorithm>
+#include <cstdlib>
 
 #include "hg_common.cuh"
 #include "hg_internal.h"
@@ -32,11 +36,13 @@
 
 namespace hg {
 
-constexpr int kIsBlock = 256;
+constexpr int kIsBlock = 512;  // consumer threads (16 warps) + 1 producer warp
+constexpr uint32_t kIsWarps = kIsBlock / 32;
 constexpr uint32_t kIsTileShift = 11;  // 2048 vertices per tile
 constexpr uint32_t kIsTile = 1u << kIsTileShift;
-constexpr uint32_t kIsVpt = kIsTile / kIsBlock;  // vertices per thread
-constexpr uint64_t kShortWork = 64;
+constexpr uint32_t kIsVpt = kIsTile / kIsBlock;  // vertices per consumer thread
+constexpr uint32_t kShort = 4;                   // short segment pair: both sides <= kShort
+constexpr int kIsStages = 2;
 
 struct IsArgs {
     const void* offa;
@@ -45,7 +51,7 @@ struct IsArgs {
     const void* kb;
     const void* va;
     const void* vb;
-    int off8a, off8b, val8a, val8b;
+    int val8a, val8b;
     uint64_t nv;
     uint64_t ntiles;
     uint32_t kcapa, kcapb;  // staged key-slice capacities (elements)
@@ -55,14 +61,9 @@ struct IsArgs {
     uint64_t cap;
     uint64_t* totals;  // [0] match_count, [1] key_comparisons
     uint32_t* ticket;
+    int dbg;           // experiment knob (HG_IS_DBG): 1 = skip the compare phase
 };
 
-__device__ __forceinline__ uint64_t ld_off(const unsigned char* base, int off8, uint32_t i) {
-    return off8 ? reinterpret_cast<const uint64_t*>(base)[i] : reinterpret_cast<const uint32_t*>(base)[i];
-}
-__device__ __forceinline__ uint64_t ld_goff(const void* p, int off8, uint64_t i) {
-    return off8 ? static_cast<const uint64_t*>(p)[i] : static_cast<const uint32_t*>(p)[i];
-}
 __device__ __forceinline__ uint64_t ld_val(const void* p, int val8, uint64_t i) {
     return val8 ? static_cast<const uint64_t*>(p)[i] : static_cast<const uint32_t*>(p)[i];
 }
@@ -71,254 +72,476 @@ __device__ __forceinline__ void st_pair(void* pairs, int pair8, uint64_t slot, u
     else reinterpret_cast<uint2*>(pairs)[slot] = make_uint2(uint32_t(l), uint32_t(r));
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+// Consumer-side wait: back off between polls so waiting warps do not steal
+// issue slots from the warps that are comparing.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try(bar, parity)) __nanosleep(64);
+}
+
+// Barrier among the kIsBlock consumer threads (the producer warp is not in it).
+__device__ __forceinline__ void consumer_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kIsBlock) : "memory");
+}
+
 __host__ __device__ inline size_t is_span_bytes(size_t bytes) { return (bytes + 32 + 15) & ~size_t(15); }
 
-template <typename K>
-__host__ __device__ inline size_t is_smem_bytes(int off8a, int off8b, uint32_t kcapa, uint32_t kcapb) {
-    return is_span_bytes(size_t(kIsTile + 1) * (off8a ? 8 : 4)) +
-           is_span_bytes(size_t(kIsTile + 1) * (off8b ? 8 : 4)) +
-           is_span_bytes(size_t(kcapa) * sizeof(K)) + is_span_bytes(size_t(kcapb) * sizeof(K));
-}
-
-// Block-wide exclusive sum of one u64 per thread; returns the thread's
-// exclusive prefix and the block total in *total.
-__device__ __forceinline__ uint64_t block_exclusive_u64(uint64_t x, uint64_t* s_warp, uint64_t* total) {
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t inc = warp_inclusive_sum(x);
-    if (lane == 31) s_warp[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-        const uint64_t w = lane < kIsBlock / 32 ? s_warp[lane] : 0;
-        const uint64_t wi = warp_inclusive_sum(w);
-        if (lane < kIsBlock / 32) s_warp[lane] = wi - w;
-        if (lane == 31) s_warp[kIsBlock / 32] = wi;
+template <typename K, typename OA, typename OB>
+struct IsLayout {
+    __host__ __device__ static size_t offa() { return is_span_bytes(size_t(kIsTile + 1) * sizeof(OA)); }
+    __host__ __device__ static size_t offb() { return is_span_bytes(size_t(kIsTile + 1) * sizeof(OB)); }
+    __host__ __device__ static size_t keys(uint32_t cap) { return is_span_bytes(size_t(cap) * sizeof(K)); }
+    __host__ __device__ static size_t stage(uint32_t kcapa, uint32_t kcapb) {
+        return offa() + offb() + keys(kcapa) + keys(kcapb);
     }
-    __syncthreads();
-    const uint64_t r = s_warp[warp] + inc - x;
-    *total = s_warp[kIsBlock / 32];
-    return r;
+};
+
+// Per-stage tile descriptor written by the producer before it arrives on the
+// stage's full barrier (release), read by consumers after their wait (acquire).
+struct TileInfo {
+    uint64_t tile;
+    uint64_t ta, tb;    // first A / B entry of the tile
+    uint32_t oa, ob;    // byte offsets of the offsets slices inside their buffers
+    uint32_t oka, okb;  // byte offsets of the key slices
+    uint32_t sta, stb;  // key slice staged in shared memory (else read from global)
+};
+
+// Segment pair of tile-local vertex v relative to the tile's key slices.
+template <typename OA, typename OB>
+struct Seg {
+    OA a0, la;
+    OB b0, lb;
+};
+
+template <typename OA, typename OB>
+__device__ __forceinline__ Seg<OA, OB> seg_of(const OA* soa, const OB* sob, uint32_t v, OA ta, OB tb) {
+    Seg<OA, OB> s;
+    const OA x0 = soa[v], x1 = soa[v + 1];
+    const OB y0 = sob[v], y1 = sob[v + 1];
+    s.a0 = x0 - ta;
+    s.la = x1 - x0;
+    s.b0 = y0 - tb;
+    s.lb = y1 - y0;
+    return s;
 }
 
-template <typename K, bool PAIRS>
-__global__ void __launch_bounds__(kIsBlock)
+// Short segment pair (both sides <= kShort): the B side is preloaded into
+// registers under predicates, then each A entry is compared against it.
+// When EMIT, matches are written in (A position, B position) order from
+// slot `sl`; ga0 / gb0 are the pair's first global entry indices.
+template <typename K, bool EMIT>
+__device__ __forceinline__ uint32_t short_pair(const K* __restrict__ pa, uint32_t la,
+                                               const K* __restrict__ pb, uint32_t lb, uint64_t sl,
+                                               const IsArgs& a, uint64_t ga0, uint64_t gb0) {
+    K kb[kShort];
+    bool in[kShort];
+#pragma unroll
+    for (uint32_t q = 0; q < kShort; ++q) {
+        in[q] = q < lb;
+        kb[q] = in[q] ? pb[q] : K(0);
+    }
+    uint32_t c = 0;
+    for (uint32_t i = 0; i < la; ++i) {
+        const K x = pa[i];
+#pragma unroll
+        for (uint32_t q = 0; q < kShort; ++q) {
+            const bool hit = in[q] && x == kb[q];
+            if constexpr (EMIT) {
+                if (hit) {
+                    if (sl < a.cap)
+                        st_pair(a.pairs, a.pair8, sl, ld_val(a.va, a.val8a, ga0 + i),
+                                ld_val(a.vb, a.val8b, gb0 + q));
+                    ++sl;
+                }
+            }
+            c += hit;
+        }
+    }
+    return c;
+}
+
+// -1 when x == y and `in` (0 otherwise): one ISETP + SEL, no dependency
+// chain through the running count (summed with IADD3).
+template <typename K>
+__device__ __forceinline__ uint32_t eq_and(K x, K y, bool in) {
+    uint32_t d;
+    if constexpr (sizeof(K) == 4) {
+        asm("{.reg .pred p; setp.ne.u32 p, %3, 0; set.eq.and.u32.u32 %0, %1, %2, p;}"
+            : "=r"(d)
+            : "r"(x), "r"(y), "r"(uint32_t(in)));
+    } else {
+        asm("{.reg .pred p; setp.ne.u32 p, %3, 0; set.eq.and.u32.u64 %0, %1, %2, p;}"
+            : "=r"(d)
+            : "l"(x), "l"(y), "r"(uint32_t(in)));
+    }
+    return d;
+}
+
+// Count-only segment pair with the inner side <= kShort entries (preloaded
+// under predicates) and an outer side of any (small) length.
+template <typename K>
+__device__ __forceinline__ uint32_t short_count(const K* __restrict__ po, uint32_t lo,
+                                                const K* __restrict__ pi, uint32_t li) {
+    K kb[kShort];
+    bool in[kShort];
+#pragma unroll
+    for (uint32_t q = 0; q < kShort; ++q) {
+        in[q] = q < li;
+        kb[q] = in[q] ? pi[q] : K(0);
+    }
+    uint32_t neg = 0;
+    for (uint32_t i = 0; i < lo; ++i) {
+        const K x = po[i];
+        neg += eq_and(x, kb[0], in[0]) + eq_and(x, kb[1], in[1]) + eq_and(x, kb[2], in[2]) +
+               eq_and(x, kb[3], in[3]);
+    }
+    return 0u - neg;
+}
+
+// Long segment pair (a0, la, b0, lb already broadcast): the |A|*|B|
+// comparisons are flattened (p = i*lb + q) and strided over the warp.
+// Returns the warp-total match count (all lanes); when EMIT, pairs go to
+// consecutive slots from `sl` in p order (ballot + popc ranks).
+template <typename K, bool EMIT>
+__device__ __forceinline__ uint64_t long_pair(const K* __restrict__ kpa, const K* __restrict__ kpb,
+                                              uint64_t a0, uint64_t la, uint64_t b0, uint64_t lb,
+                                              uint64_t sl, const IsArgs& a, uint64_t ta, uint64_t tb) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t work = la * lb;
+    uint64_t c = 0;
+    auto loop = [&](auto work_t) {
+        using I = decltype(work_t);
+        const I w = I(work), l = I(lb);
+        if constexpr (!EMIT) {
+            for (I p = lane; p < w; p += 32) {
+                const I i = p / l, q = p - i * l;
+                c += kpa[a0 + i] == kpb[b0 + q];
+            }
+        } else {
+            for (I p0 = 0; p0 < w && sl < a.cap; p0 += 32) {
+                const I p = p0 + lane;
+                I i = 0, q = 0;
+                bool hit = false;
+                if (p < w) {
+                    i = p / l;
+                    q = p - i * l;
+                    hit = kpa[a0 + i] == kpb[b0 + q];
+                }
+                const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+                const uint64_t my = sl + __popc(hm & lanemask_lt());
+                if (hit && my < a.cap)
+                    st_pair(a.pairs, a.pair8, my, ld_val(a.va, a.val8a, ta + a0 + i),
+                            ld_val(a.vb, a.val8b, tb + b0 + q));
+                sl += __popc(hm);
+                if (lane == 0) c += __popc(hm);
+            }
+        }
+    };
+    if (work + 32 < (uint64_t(1) << 32)) loop(uint32_t(0));
+    else loop(uint64_t(0));
+    return warp_sum(c);
+}
+
+// One tile, consumer side. kpa / kpb point at the tile's key slices (shared
+// memory when staged: the instantiation with shared pointers compiles to LDS).
+// Count mode accumulates into matches / compared; pairs mode also writes the
+// tile's pairs (needs the consumer barrier and the look-back).
+template <typename K, typename OA, typename OB, bool PAIRS>
+__device__ __forceinline__ void intersect_tile(const IsArgs& a, const OA* soa, const OB* sob,
+                                               const K* kpa, const K* kpb, uint64_t tile,
+                                               uint64_t ta, uint64_t tb, uint64_t& matches,
+                                               uint64_t& compared, uint32_t (*s_cnt)[kIsBlock],
+                                               uint64_t* s_wt, uint64_t* s_base,
+                                               uint32_t (*s_q)[kIsVpt * 32]) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t vb = tile << kIsTileShift;
+    const uint32_t pv = uint32_t(a.nv - vb < kIsTile ? a.nv - vb : uint64_t(kIsTile));
+    const OA tA = OA(ta);
+    const OB tB = OB(tb);
+    // Phase 1: every vertex's segment pair; comparisons; compact the vertices
+    // with both sides non-empty (~40% at load 1) into this warp's queue, so
+    // the compare loops run densely instead of over 60% idle lanes.
+    uint32_t* const q = s_q[warp];
+    uint32_t nq = 0;
+    uint64_t cmp_tile = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < kIsVpt; ++j) {
+        const uint32_t v = j * kIsBlock + tid;
+        Seg<OA, OB> sp{0, 0, 0, 0};
+        if (v < pv) sp = seg_of(soa, sob, v, tA, tB);
+        cmp_tile += uint64_t(sp.la) * uint64_t(sp.lb);
+        const bool act = sp.la && sp.lb;
+        const uint32_t m = __ballot_sync(0xffffffffu, act);
+        if (act) q[nq + __popc(m & lanemask_lt())] = v;
+        nq += __popc(m);
+        if constexpr (PAIRS) s_cnt[j][tid] = 0;
+    }
+    __syncwarp();
+    // Phase 2: the queued segment pairs, 32 at a time. Pairs mode re-queues
+    // (in place) the vertices that matched, for the write pass.
+    compared += cmp_tile;
+    uint32_t nq2 = 0;
+    if (a.dbg == 1) nq = 0;
+    for (uint32_t k0 = 0; k0 < nq; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        const bool act = k < nq;
+        const uint32_t v = act ? q[k] : 0;
+        Seg<OA, OB> sp{0, 0, 0, 0};
+        if (act) sp = seg_of(soa, sob, v, tA, tB);
+        // short classes: B side <= kShort with A <= 2*kShort (A outer), or,
+        // counting only, A side <= kShort with B <= 2*kShort (B outer)
+        const bool sb = sp.lb <= kShort && sp.la <= 2 * kShort;
+        const bool sa = !PAIRS && !sb && sp.la <= kShort && sp.lb <= 2 * kShort;
+        const bool lg = act && !sb && !sa;
+        uint32_t c = 0;
+        if (act && sb) {
+            if constexpr (PAIRS)
+                c = short_pair<K, false>(kpa + sp.a0, uint32_t(sp.la), kpb + sp.b0, uint32_t(sp.lb), 0, a, 0, 0);
+            else
+                c = short_count<K>(kpa + sp.a0, uint32_t(sp.la), kpb + sp.b0, uint32_t(sp.lb));
+        } else if (act && sa) {
+            c = short_count<K>(kpb + sp.b0, uint32_t(sp.lb), kpa + sp.a0, uint32_t(sp.la));
+        }
+        uint32_t wl = __ballot_sync(0xffffffffu, lg);
+        while (wl) {
+            const int src = __ffs(wl) - 1;
+            wl &= wl - 1;
+            const uint64_t cl = long_pair<K, false>(
+                kpa, kpb, __shfl_sync(0xffffffffu, uint64_t(sp.a0), src),
+                __shfl_sync(0xffffffffu, uint64_t(sp.la), src), __shfl_sync(0xffffffffu, uint64_t(sp.b0), src),
+                __shfl_sync(0xffffffffu, uint64_t(sp.lb), src), 0, a, ta, tb);
+            if (int(lane) == src) c = uint32_t(cl);
+        }
+        if constexpr (PAIRS) {
+            if (c) s_cnt[v / kIsBlock][v % kIsBlock] = c;
+            const uint32_t mm = __ballot_sync(0xffffffffu, c != 0);
+            __syncwarp();
+            if (c) q[nq2 + __popc(mm & lanemask_lt())] = v;
+            nq2 += __popc(mm);
+            __syncwarp();
+        } else {
+            matches += c;
+        }
+    }
+    if constexpr (PAIRS) {
+        // exclusive rank of each (j, tid) in vertex order j*kIsBlock + tid
+        __syncwarp();
+#pragma unroll
+        for (uint32_t j = 0; j < kIsVpt; ++j) {
+            const uint32_t c = s_cnt[j][tid];
+            const uint32_t inc = warp_inclusive_sum(c);
+            s_cnt[j][tid] = inc - c;  // warp-exclusive
+            if (lane == 31) s_wt[j * kIsWarps + warp] = inc;
+            matches += c;
+        }
+        consumer_sync();
+        constexpr uint32_t kPer = kIsVpt * kIsWarps / 32;  // (j, warp) totals per lane
+        static_assert(kPer >= 1 && kIsVpt * kIsWarps == 32 * kPer, "scan layout");
+        if (warp == 0) {
+            uint64_t x[kPer], sum = 0;
+#pragma unroll
+            for (uint32_t e = 0; e < kPer; ++e) sum += (x[e] = s_wt[kPer * lane + e]);
+            const uint64_t inc = warp_inclusive_sum(sum);
+            uint64_t run = inc - sum;
+#pragma unroll
+            for (uint32_t e = 0; e < kPer; ++e) {
+                s_wt[kPer * lane + e] = run;
+                run += x[e];
+            }
+            const uint64_t tile_total = __shfl_sync(0xffffffffu, inc, 31);
+            // decoupled look-back over tiles (ticket order = tile order)
+            uint64_t prefix = 0;
+            if (tile == 0) {
+                if (lane == 0) st_relaxed_u64(a.status, kScanFlagIncl | tile_total);
+            } else {
+                if (lane == 0) st_relaxed_u64(a.status + tile, kScanFlagAgg | tile_total);
+                int64_t idx = int64_t(tile) - 1;
+                while (true) {
+                    const int64_t jj = idx - int64_t(lane);
+                    uint64_t sw = kScanFlagIncl;
+                    if (jj >= 0) {
+                        do {
+                            sw = ld_relaxed_u64(a.status + jj);
+                        } while ((sw >> 62) == 0);
+                    }
+                    const uint32_t inclm = __ballot_sync(0xffffffffu, (sw >> 62) == 2);
+                    const uint32_t stop = inclm ? uint32_t(__ffs(inclm) - 1) : 32u;
+                    prefix += warp_sum(lane <= stop ? (sw & kScanValMask) : uint64_t(0));
+                    if (inclm) break;
+                    idx -= 32;
+                }
+                if (lane == 0) st_relaxed_u64(a.status + tile, kScanFlagIncl | (prefix + tile_total));
+            }
+            if (lane == 0) {
+                s_base[0] = prefix;
+                s_base[1] = tile_total;
+            }
+        }
+        consumer_sync();
+        const uint64_t tbase = s_base[0];
+        if (tbase < a.cap && s_base[1]) {
+            // write pass over the re-queued matching vertices
+            for (uint32_t k0 = 0; k0 < nq2; k0 += 32) {
+                const uint32_t k = k0 + lane;
+                const bool act = k < nq2;
+                const uint32_t v = act ? q[k] : 0;
+                const uint32_t j = v / kIsBlock, t = v % kIsBlock;
+                const uint64_t slot = tbase + s_wt[j * kIsWarps + warp] + s_cnt[j][t];
+                Seg<OA, OB> sp{0, 0, 0, 0};
+                if (act) sp = seg_of(soa, sob, v, tA, tB);
+                const bool go = act && slot < a.cap;
+                const bool lg = !(sp.lb <= kShort && sp.la <= 2 * kShort);
+                if (go && !lg)
+                    short_pair<K, true>(kpa + sp.a0, uint32_t(sp.la), kpb + sp.b0, uint32_t(sp.lb), slot,
+                                        a, ta + sp.a0, tb + sp.b0);
+                uint32_t wm = __ballot_sync(0xffffffffu, go && lg);
+                while (wm) {
+                    const int src = __ffs(wm) - 1;
+                    wm &= wm - 1;
+                    long_pair<K, true>(kpa, kpb, __shfl_sync(0xffffffffu, uint64_t(sp.a0), src),
+                                       __shfl_sync(0xffffffffu, uint64_t(sp.la), src),
+                                       __shfl_sync(0xffffffffu, uint64_t(sp.b0), src),
+                                       __shfl_sync(0xffffffffu, uint64_t(sp.lb), src),
+                                       __shfl_sync(0xffffffffu, slot, src), a, ta, tb);
+                }
+            }
+        }
+    }
+}
+
+template <typename K, typename OA, typename OB, bool PAIRS>
+__global__ void __launch_bounds__(kIsBlock + 32, 2)
 k_intersect(IsArgs a) {
+    using L = IsLayout<K, OA, OB>;
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ uint64_t s_bar;
-    __shared__ uint64_t s_tile, s_ta, s_tb, s_na, s_nb, s_base;
-    __shared__ uint32_t s_oa, s_ob, s_oka, s_okb, s_sta, s_stb;
-    __shared__ uint64_t s_warp[kIsBlock / 32 + 1];
-    const uint32_t tid = threadIdx.x, lane = tid & 31;
-    const size_t offa_bytes = is_span_bytes(size_t(kIsTile + 1) * (a.off8a ? 8 : 4));
-    const size_t offb_bytes = is_span_bytes(size_t(kIsTile + 1) * (a.off8b ? 8 : 4));
-    unsigned char* const b_oa = smem;
-    unsigned char* const b_ob = b_oa + offa_bytes;
-    unsigned char* const b_ka = b_ob + offb_bytes;
-    unsigned char* const b_kb = b_ka + is_span_bytes(size_t(a.kcapa) * sizeof(K));
+    __shared__ uint64_t s_full[kIsStages], s_empty[kIsStages];
+    __shared__ TileInfo s_info[kIsStages];
+    __shared__ uint64_t s_base[2];
+    __shared__ uint64_t s_wt[kIsVpt * kIsWarps];
+    __shared__ uint32_t s_cnt[PAIRS ? kIsVpt : 1][kIsBlock];
+    __shared__ uint32_t s_q[kIsWarps][kIsVpt * 32];  // per-warp queues of tile-local vertices
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const size_t stage_bytes = L::stage(a.kcapa, a.kcapb);
     if (tid == 0) {
-        mbar_init(&s_bar, 1);
+        for (int st = 0; st < kIsStages; ++st) {
+            mbar_init(&s_full[st], 1);
+            mbar_init(&s_empty[st], kIsWarps);
+        }
         fence_mbar_init();
     }
-    uint32_t phase = 0;
-    uint64_t matches = 0, compared = 0;
-    while (true) {
-        if (tid == 0) {
-            const uint64_t p = atomicAdd(a.ticket, 1u);
-            s_tile = p;
-            if (p < a.ntiles) {
+    __syncthreads();
+
+    if (warp == kIsWarps) {
+        // ---------------- producer (one thread)
+        if (lane == 0) {
+            const OA* offa = static_cast<const OA*>(a.offa);
+            const OB* offb = static_cast<const OB*>(a.offb);
+            for (uint32_t it = 0;; ++it) {
+                const int st = int(it % kIsStages);
+                if (it >= uint32_t(kIsStages)) mbar_wait(&s_empty[st], ((it / kIsStages) - 1) & 1);
+                TileInfo& ti = s_info[st];
+                const uint64_t p = atomicAdd(a.ticket, 1u);
+                ti.tile = p;
+                if (p >= a.ntiles) {
+                    mbar_arrive(&s_full[st]);
+                    break;
+                }
+                unsigned char* const b_oa = smem + st * stage_bytes;
+                unsigned char* const b_ob = b_oa + L::offa();
+                unsigned char* const b_ka = b_ob + L::offb();
+                unsigned char* const b_kb = b_ka + L::keys(a.kcapa);
                 const uint64_t vb = p << kIsTileShift;
                 const uint32_t pv = uint32_t(a.nv - vb < kIsTile ? a.nv - vb : uint64_t(kIsTile));
-                const uint64_t ta = ld_goff(a.offa, a.off8a, vb), tae = ld_goff(a.offa, a.off8a, vb + pv);
-                const uint64_t tb = ld_goff(a.offb, a.off8b, vb), tbe = ld_goff(a.offb, a.off8b, vb + pv);
-                s_ta = ta; s_tb = tb; s_na = tae - ta; s_nb = tbe - tb;
-                const uint32_t sta = tae - ta <= a.kcapa, stb = tbe - tb <= a.kcapb;
-                s_sta = sta; s_stb = stb;
-                fence_proxy_async();
+                const uint64_t ta = offa[vb], tae = offa[vb + pv];
+                const uint64_t tb = offb[vb], tbe = offb[vb + pv];
+                ti.ta = ta;
+                ti.tb = tb;
+                ti.sta = tae - ta <= a.kcapa;
+                ti.stb = tbe - tb <= a.kcapb;
                 auto span = [](uintptr_t ad, size_t bytes, uint32_t& lo_off) -> uint32_t {
                     const uintptr_t lo = ad & ~uintptr_t(15), hi = (ad + bytes + 15) & ~uintptr_t(15);
                     lo_off = uint32_t(ad - lo);
                     return uint32_t(hi - lo);
                 };
-                const int oba = a.off8a ? 8 : 4, obb = a.off8b ? 8 : 4;
-                const uintptr_t aoa = reinterpret_cast<uintptr_t>(a.offa) + vb * oba;
-                const uintptr_t aob = reinterpret_cast<uintptr_t>(a.offb) + vb * obb;
+                const uintptr_t aoa = reinterpret_cast<uintptr_t>(offa + vb);
+                const uintptr_t aob = reinterpret_cast<uintptr_t>(offb + vb);
                 const uintptr_t aka = reinterpret_cast<uintptr_t>(static_cast<const K*>(a.ka) + ta);
                 const uintptr_t akb = reinterpret_cast<uintptr_t>(static_cast<const K*>(a.kb) + tb);
                 uint32_t oa, ob, oka = 0, okb = 0;
-                const uint32_t la = span(aoa, size_t(pv + 1) * oba, oa);
-                const uint32_t lb = span(aob, size_t(pv + 1) * obb, ob);
-                const uint32_t lka = (sta && tae > ta) ? span(aka, size_t(tae - ta) * sizeof(K), oka) : 0;
-                const uint32_t lkb = (stb && tbe > tb) ? span(akb, size_t(tbe - tb) * sizeof(K), okb) : 0;
-                s_oa = oa; s_ob = ob; s_oka = oka; s_okb = okb;
-                mbar_arrive_expect_tx(&s_bar, la + lb + lka + lkb);
-                tma_load_1d(b_oa, reinterpret_cast<const void*>(aoa - oa), la, &s_bar);
-                tma_load_1d(b_ob, reinterpret_cast<const void*>(aob - ob), lb, &s_bar);
-                if (lka) tma_load_1d(b_ka, reinterpret_cast<const void*>(aka - oka), lka, &s_bar);
-                if (lkb) tma_load_1d(b_kb, reinterpret_cast<const void*>(akb - okb), lkb, &s_bar);
+                const uint32_t la = span(aoa, size_t(pv + 1) * sizeof(OA), oa);
+                const uint32_t lb = span(aob, size_t(pv + 1) * sizeof(OB), ob);
+                const uint32_t lka = (ti.sta && tae > ta) ? span(aka, size_t(tae - ta) * sizeof(K), oka) : 0;
+                const uint32_t lkb = (ti.stb && tbe > tb) ? span(akb, size_t(tbe - tb) * sizeof(K), okb) : 0;
+                ti.oa = oa;
+                ti.ob = ob;
+                ti.oka = oka;
+                ti.okb = okb;
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&s_full[st], la + lb + lka + lkb);
+                tma_load_1d(b_oa, reinterpret_cast<const void*>(aoa - oa), la, &s_full[st]);
+                tma_load_1d(b_ob, reinterpret_cast<const void*>(aob - ob), lb, &s_full[st]);
+                if (lka) tma_load_1d(b_ka, reinterpret_cast<const void*>(aka - oka), lka, &s_full[st]);
+                if (lkb) tma_load_1d(b_kb, reinterpret_cast<const void*>(akb - okb), lkb, &s_full[st]);
             }
         }
-        __syncthreads();
-        const uint64_t tile = s_tile;
-        if (tile >= a.ntiles) break;
-        const uint64_t vb = tile << kIsTileShift;
-        const uint32_t pv = uint32_t(a.nv - vb < kIsTile ? a.nv - vb : uint64_t(kIsTile));
-        const uint64_t ta = s_ta, tb = s_tb;
-        const unsigned char* soa = b_oa + s_oa;
-        const unsigned char* sob = b_ob + s_ob;
-        const K* kpa = s_sta ? reinterpret_cast<const K*>(b_ka + s_oka) : static_cast<const K*>(a.ka) + ta;
-        const K* kpb = s_stb ? reinterpret_cast<const K*>(b_kb + s_okb) : static_cast<const K*>(a.kb) + tb;
-        mbar_wait(&s_bar, phase);
-        phase ^= 1;
-
-        // this thread's vertices [v0, v1) (tile-local)
-        const uint32_t v0 = min(tid * kIsVpt, pv), v1 = min(v0 + kIsVpt, pv);
-        uint64_t ab[kIsVpt + 1], bb[kIsVpt + 1];
-#pragma unroll
-        for (uint32_t j = 0; j <= kIsVpt; ++j) {
-            const uint32_t v = min(v0 + j, v1);
-            ab[j] = ld_off(soa, a.off8a, v) - ta;
-            bb[j] = ld_off(sob, a.off8b, v) - tb;
-        }
-        uint32_t longm = 0;
-        uint64_t cnt[PAIRS ? kIsVpt : 1];
-#pragma unroll
-        for (uint32_t j = 0; j < kIsVpt; ++j) {
-            const uint64_t la = ab[j + 1] - ab[j], lb = bb[j + 1] - bb[j];
-            const uint64_t work = la * lb;
-            compared += work;
-            uint64_t c = 0;
-            if (work <= kShortWork) {
-                for (uint64_t i = ab[j]; i < ab[j + 1]; ++i) {
-                    const K x = kpa[i];
-                    for (uint64_t q = bb[j]; q < bb[j + 1]; ++q) c += kpb[q] == x;
-                }
-            } else {
-                longm |= 1u << j;
-            }
-            if constexpr (PAIRS) cnt[j] = c;
-            else matches += c;
-        }
-        // long segment pairs: flattened p = i*lb + q, strided over the warp
-#pragma unroll
-        for (uint32_t j = 0; j < kIsVpt; ++j) {
-            uint32_t wm = __ballot_sync(0xffffffffu, (longm >> j) & 1u);
-            while (wm) {
-                const int src = __ffs(wm) - 1;
-                wm &= wm - 1;
-                const uint64_t a0 = __shfl_sync(0xffffffffu, ab[j], src);
-                const uint64_t la = __shfl_sync(0xffffffffu, ab[j + 1], src) - a0;
-                const uint64_t b0 = __shfl_sync(0xffffffffu, bb[j], src);
-                const uint64_t lb = __shfl_sync(0xffffffffu, bb[j + 1], src) - b0;
-                const uint64_t work = la * lb;
-                uint64_t c = 0;
-                for (uint64_t p = lane; p < work; p += 32) {
-                    const uint64_t i = p / lb, q = p - i * lb;
-                    c += kpa[a0 + i] == kpb[b0 + q];
-                }
-                if constexpr (PAIRS) {
-                    c = warp_sum(c);
-                    if (int(lane) == src) cnt[j] = c;
-                } else {
-                    matches += c;
-                }
-            }
-        }
-        if constexpr (PAIRS) {
-            uint64_t mine = 0;
-#pragma unroll
-            for (uint32_t j = 0; j < kIsVpt; ++j) mine += cnt[j];
-            matches += mine;
-            uint64_t tile_total;
-            const uint64_t excl = block_exclusive_u64(mine, s_warp, &tile_total);
-            // decoupled look-back over tiles (ticket order = tile order)
-            if (tid < 32) {
-                uint64_t prefix = 0;
-                if (tile == 0) {
-                    if (lane == 0) st_relaxed_u64(a.status, kScanFlagIncl | tile_total);
-                } else {
-                    if (lane == 0) st_relaxed_u64(a.status + tile, kScanFlagAgg | tile_total);
-                    int64_t idx = int64_t(tile) - 1;
-                    while (true) {
-                        const int64_t jj = idx - int64_t(lane);
-                        uint64_t s = kScanFlagIncl;
-                        if (jj >= 0) {
-                            do {
-                                s = ld_relaxed_u64(a.status + jj);
-                            } while ((s >> 62) == 0);
-                        }
-                        const uint32_t incl = __ballot_sync(0xffffffffu, (s >> 62) == 2);
-                        const uint32_t stop = incl ? uint32_t(__ffs(incl) - 1) : 32u;
-                        prefix += warp_sum(lane <= stop ? (s & kScanValMask) : uint64_t(0));
-                        if (incl) break;
-                        idx -= 32;
-                    }
-                    if (lane == 0) st_relaxed_u64(a.status + tile, kScanFlagIncl | (prefix + tile_total));
-                }
-                if (lane == 0) s_base = prefix;
-            }
-            __syncthreads();
-            const uint64_t tbase = s_base;
-            if (tbase < a.cap) {
-                uint64_t slot = tbase + excl;
-#pragma unroll
-                for (uint32_t j = 0; j < kIsVpt; ++j) {
-                    if (!((longm >> j) & 1u) && cnt[j]) {
-                        uint64_t sl = slot;
-                        for (uint64_t i = ab[j]; i < ab[j + 1] && sl < a.cap; ++i) {
-                            const K x = kpa[i];
-                            for (uint64_t q = bb[j]; q < bb[j + 1]; ++q) {
-                                if (kpb[q] == x && sl < a.cap) {
-                                    st_pair(a.pairs, a.pair8, sl, ld_val(a.va, a.val8a, ta + i),
-                                            ld_val(a.vb, a.val8b, tb + q));
-                                    ++sl;
-                                }
-                            }
-                        }
-                    }
-                    uint32_t wm = __ballot_sync(0xffffffffu, ((longm >> j) & 1u) && cnt[j] && slot < a.cap);
-                    while (wm) {
-                        const int src = __ffs(wm) - 1;
-                        wm &= wm - 1;
-                        const uint64_t a0 = __shfl_sync(0xffffffffu, ab[j], src);
-                        const uint64_t la = __shfl_sync(0xffffffffu, ab[j + 1], src) - a0;
-                        const uint64_t b0 = __shfl_sync(0xffffffffu, bb[j], src);
-                        const uint64_t lb = __shfl_sync(0xffffffffu, bb[j + 1], src) - b0;
-                        uint64_t ws = __shfl_sync(0xffffffffu, slot, src);
-                        const uint64_t work = la * lb;
-                        for (uint64_t p0 = 0; p0 < work && ws < a.cap; p0 += 32) {
-                            const uint64_t p = p0 + lane;
-                            uint64_t i = 0, q = 0;
-                            bool hit = false;
-                            if (p < work) {
-                                i = p / lb;
-                                q = p - i * lb;
-                                hit = kpa[a0 + i] == kpb[b0 + q];
-                            }
-                            const uint32_t hm = __ballot_sync(0xffffffffu, hit);
-                            const uint64_t my = ws + __popc(hm & lanemask_lt());
-                            if (hit && my < a.cap)
-                                st_pair(a.pairs, a.pair8, my, ld_val(a.va, a.val8a, ta + a0 + i),
-                                        ld_val(a.vb, a.val8b, tb + b0 + q));
-                            ws += __popc(hm);
-                        }
-                    }
-                    slot += cnt[j];
-                }
-            }
-        }
-        __syncthreads();
+        return;
     }
-    // block reduction -> one pair of u64 atomics per CTA
-    __shared__ unsigned long long s_m[kIsBlock / 32], s_c[kIsBlock / 32];
+
+    // ---------------- consumers
+    uint64_t matches = 0, compared = 0;
+    for (uint32_t it = 0;; ++it) {
+        const int st = int(it % kIsStages);
+        mbar_wait_backoff(&s_full[st], (it / kIsStages) & 1);
+        const TileInfo& ti = s_info[st];
+        const uint64_t tile = ti.tile;
+        if (tile >= a.ntiles) break;
+        unsigned char* const b_oa = smem + st * stage_bytes;
+        const OA* soa = reinterpret_cast<const OA*>(b_oa + ti.oa);
+        const OB* sob = reinterpret_cast<const OB*>(b_oa + L::offa() + ti.ob);
+        const K* ska = reinterpret_cast<const K*>(b_oa + L::offa() + L::offb() + ti.oka);
+        const K* skb = reinterpret_cast<const K*>(b_oa + L::offa() + L::offb() + L::keys(a.kcapa) + ti.okb);
+        const uint64_t ta = ti.ta, tb = ti.tb;
+        if (ti.sta && ti.stb) {
+            intersect_tile<K, OA, OB, PAIRS>(a, soa, sob, ska, skb, tile, ta, tb, matches, compared,
+                                             s_cnt, s_wt, s_base, s_q);
+        } else {
+            const K* gka = static_cast<const K*>(a.ka) + ta;
+            const K* gkb = static_cast<const K*>(a.kb) + tb;
+            intersect_tile<K, OA, OB, PAIRS>(a, soa, sob, ti.sta ? ska : gka, ti.stb ? skb : gkb, tile,
+                                             ta, tb, matches, compared, s_cnt, s_wt, s_base, s_q);
+        }
+        // release the stage to the producer
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[st]);
+        if constexpr (PAIRS) consumer_sync();  // s_cnt / s_wt / s_base reuse
+    }
+    // block reduction over the consumers -> one pair of u64 atomics per CTA
+    __shared__ unsigned long long s_m[kIsWarps], s_c[kIsWarps];
     matches = warp_sum(matches);
     compared = warp_sum(compared);
     if (lane == 0) {
-        s_m[tid >> 5] = matches;
-        s_c[tid >> 5] = compared;
+        s_m[warp] = matches;
+        s_c[warp] = compared;
     }
-    __syncthreads();
+    consumer_sync();
     if (tid < 32) {
-        unsigned long long x = tid < kIsBlock / 32 ? s_m[tid] : 0;
-        unsigned long long y = tid < kIsBlock / 32 ? s_c[tid] : 0;
+        unsigned long long x = tid < kIsWarps ? s_m[tid] : 0;
+        unsigned long long y = tid < kIsWarps ? s_c[tid] : 0;
         x = warp_sum(x);
         y = warp_sum(y);
         if (tid == 0) {
@@ -328,7 +551,7 @@ k_intersect(IsArgs a) {
     }
 }
 
-template <typename K>
+template <typename K, typename OA, typename OB>
 static cudaError_t intersect_impl(const TableDesc& A, const TableDesc& B, const IntersectArgs& ia,
                                   cudaStream_t s) {
     IsArgs a{};
@@ -338,8 +561,6 @@ static cudaError_t intersect_impl(const TableDesc& A, const TableDesc& B, const 
     a.kb = B.keys;
     a.va = A.vals;
     a.vb = B.vals;
-    a.off8a = A.off_bytes == 8;
-    a.off8b = B.off_bytes == 8;
     a.val8a = A.val_bytes == 8;
     a.val8b = B.val_bytes == 8;
     a.nv = A.nv;
@@ -348,17 +569,19 @@ static cudaError_t intersect_impl(const TableDesc& A, const TableDesc& B, const 
     a.pair8 = ia.pair_bytes == 8;
     a.cap = ia.pairs ? ia.cap : 0;
     a.totals = ia.totals;
-    // staged key capacity per side: ~1.5x the mean slice + slack, within a
-    // ~100 KB per-CTA budget (2+ CTAs per SM); larger slices read global memory
+    a.dbg = getenv("HG_IS_DBG") ? atoi(getenv("HG_IS_DBG")) : 0;
+    // staged key capacity per side: ~1.25x the mean slice + slack (a uniform
+    // tile exceeds it with negligible probability), within a 12 KB per side
+    // and stage budget; larger slices are read from global memory
     auto capfor = [&](uint64_t n) {
         const double mean = double(n) * double(kIsTile) / double(A.nv);
-        const double lim = double((size_t(40) << 10) / sizeof(K));
-        return uint32_t(std::min(lim, std::max(256.0, 1.5 * mean + 256.0)));
+        const double lim = double((size_t(12) << 10) / sizeof(K));
+        return uint32_t(std::min(lim, std::max(128.0, 1.25 * mean + 128.0)));
     };
     a.kcapa = capfor(A.n);
     a.kcapb = capfor(B.n);
     const bool pairs = ia.pairs != nullptr && ia.cap > 0;
-    const size_t smem = is_smem_bytes<K>(a.off8a, a.off8b, a.kcapa, a.kcapb);
+    const size_t smem = kIsStages * IsLayout<K, OA, OB>::stage(a.kcapa, a.kcapb);
     const size_t st_bytes = pairs ? a.ntiles * sizeof(uint64_t) : 0;
     void* scratch = nullptr;
     cudaError_t e = cudaMallocAsync(&scratch, st_bytes + 16, s);
@@ -367,26 +590,35 @@ static cudaError_t intersect_impl(const TableDesc& A, const TableDesc& B, const 
     a.ticket = reinterpret_cast<uint32_t*>(static_cast<char*>(scratch) + st_bytes);
     do {
         if ((e = cudaMemsetAsync(scratch, 0, st_bytes + 16, s)) != cudaSuccess) break;
-        auto kern = pairs ? k_intersect<K, true> : k_intersect<K, false>;
+        auto kern = pairs ? k_intersect<K, OA, OB, true> : k_intersect<K, OA, OB, false>;
         if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) !=
             cudaSuccess)
             break;
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kIsBlock, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kIsBlock + 32, smem);
         const unsigned grid = unsigned(std::max<uint64_t>(
             1, std::min<uint64_t>(uint64_t(std::max(1, per_sm)) * num_sms(), a.ntiles)));
         HG_LAUNCH(pairs ? "k12_intersect_pairs" : "k12_intersect", s,
-                  kern<<<grid, kIsBlock, smem, s>>>(a));
+                  kern<<<grid, kIsBlock + 32, smem, s>>>(a));
         e = cudaGetLastError();
     } while (false);
     cudaFreeAsync(scratch, s);
     return e;
 }
 
+template <typename K>
+static cudaError_t intersect_off(const TableDesc& A, const TableDesc& B, const IntersectArgs& ia,
+                                 cudaStream_t s) {
+    if (A.off_bytes == 4 && B.off_bytes == 4) return intersect_impl<K, uint32_t, uint32_t>(A, B, ia, s);
+    if (A.off_bytes == 8 && B.off_bytes == 8) return intersect_impl<K, uint64_t, uint64_t>(A, B, ia, s);
+    if (A.off_bytes == 4) return intersect_impl<K, uint32_t, uint64_t>(A, B, ia, s);
+    return intersect_impl<K, uint64_t, uint32_t>(A, B, ia, s);
+}
+
 cudaError_t intersect_tables(const TableDesc& A, const TableDesc& B, const IntersectArgs& ia,
                              cudaStream_t s) {
     if (A.key_bytes != B.key_bytes || A.nv != B.nv) return cudaErrorInvalidValue;
-    return A.key_bytes == 4 ? intersect_impl<uint32_t>(A, B, ia, s) : intersect_impl<uint64_t>(A, B, ia, s);
+    return A.key_bytes == 4 ? intersect_off<uint32_t>(A, B, ia, s) : intersect_off<uint64_t>(A, B, ia, s);
 }
 
 }  // namespace hg

@@ -17,10 +17,14 @@ hg.generate(probes, kind=0, seed=2)
 res = torch.zeros(2, dtype=torch.int64, device="cuda")
 ta = hg.build_v2(keys)
 tb = hg.build_v2(probes, vertex_count=ta.num_vertices())
-for _ in range(3):
-    hg.probe_new_device(ta, tb, res)
 pairs = torch.empty((1 << 25, 2), dtype=torch.int32, device="cuda")
-for _ in range(2):
+e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+for _ in range(3):
+    e0.record()
+    hg.probe_new_device(ta, tb, res)
+    e1.record()
     hg.probe_new_device(ta, tb, res, pairs=pairs, pair_width=4, pair_cap=1 << 25)
-torch.cuda.synchronize()
+    e2.record()
+    torch.cuda.synchronize()
+    print(f"intersect count {e0.elapsed_time(e1):.3f} ms, pairs {e1.elapsed_time(e2):.3f} ms")
 print("matches", res.tolist())
