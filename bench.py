@@ -216,6 +216,68 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ secondary configs
+
+def _timed(torch, stream, fn, reps=3):
+    """Average ms of fn() over reps (after one untimed call), CUDA events on `stream`."""
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def bench_c3(torch, hg, stream, sp, log2n=28):
+    """C3: 2^28 u64 keys ~ Zipf(s = 1.0) over 2^24 ranks with u64 values,
+    binned and simple builds across the load sweep (G keys/s = N / t)."""
+    n = 1 << log2n
+    cdf = torch.tensor(hg.zipf_cdf(1 << 24, 1.0), dtype=torch.float64, device="cuda")
+    keys = torch.empty(n, dtype=torch.int64, device="cuda")
+    hg.generate(keys, kind=3, seed=1, ref=cdf)
+    vals = torch.arange(n, dtype=torch.int64, device="cuda")
+    out = {"workload": "2^28 u64 Zipf(1.0) keys over 2^24 ranks, u64 values = position"}
+    for load in (0.5, 1.0, 1.5, 2.0, 4.0):
+        row = {}
+        for name, bfn in (("v2", hg.build_v2), ("v1", hg.build_v1)):
+            cfg = hg.BuildConfig(load_factor=load)
+            ms = _timed(torch, stream, lambda: bfn(keys, cfg, vals=vals, stream=sp).close(sp),
+                        reps=2 if name == "v1" else 3)
+            row[name] = {"build_ms": round(ms, 3), "build_gkeys_s": round(n / (ms * 1e-3) / 1e9, 3)}
+        out[f"load_{load}"] = row
+    del keys, vals
+    torch.cuda.empty_cache()
+    return out
+
+
+def bench_c4(torch, hg, stream, sp):
+    """C4: probe_standard with pairs, 2^29 probes into 2^28 unique u32 build
+    keys at hit ratio 0.1 / 0.5 / 1.0 (G probes/s = M / t, u32 pairs)."""
+    n, m = 1 << 28, 1 << 29
+    build = torch.empty(n, dtype=torch.int32, device="cuda")
+    hg.generate(build, kind=2)
+    t = hg.build_v2(build, stream=sp)
+    probes = torch.empty(m, dtype=torch.int32, device="cuda")
+    res = torch.zeros(2, dtype=torch.int64, device="cuda")
+    pairs = torch.empty((m, 2), dtype=torch.int32, device="cuda")
+    out = {"workload": "build 2^28 unique u32 (scramble31), probe 2^29 u32 with u32 pairs"}
+    for h in (0.1, 0.5, 1.0):
+        hg.generate(probes, kind=1, seed=3, hit=h, ref=build)
+        ms = _timed(torch, stream, lambda: hg.probe_device(t, probes, res, pairs=pairs,
+                                                           pair_width=4, pair_cap=m, stream=sp))
+        mc, cmp = (int(x) for x in res.cpu().tolist())
+        out[f"hit_{h}"] = {"probe_ms": round(ms, 3),
+                           "gprobes_s": round(m / (ms * 1e-3) / 1e9, 3),
+                           "match_count": mc, "key_comparisons": cmp}
+    t.close(sp)
+    del build, probes, pairs
+    torch.cuda.empty_cache()
+    return out
+
+
 # ------------------------------------------------------------------ B200 arm
 
 def run_b200(args):
@@ -365,6 +427,10 @@ def run_b200(args):
         tb = ti = 0.0
         reps = 3
         ta = hg.build_v2(keys, stream=sp)
+        warm = hg.build_v2(probes, vertex_count=nv, stream=sp)  # pool warm-up (untimed)
+        hg.probe_new_device(ta, warm, result, stream=sp)
+        warm.close(sp)
+        torch.cuda.synchronize()
         for _ in range(reps):
             e0.record(stream)
             tbl_b = hg.build_v2(probes, vertex_count=nv, stream=sp)
@@ -386,6 +452,8 @@ def run_b200(args):
                                              * 1e-3) / 1e9, 3),
             "match_count": pn_matches, "key_comparisons": pn_cmp,
             "matches_equal_probe_standard": pn_matches == matches}
+        extras["c3_zipf"] = bench_c3(torch, hg, stream, sp)
+        extras["c4_join"] = bench_c4(torch, hg, stream, sp)
         line["phases"] = extras
 
     # ---- e2e through the public API with pinned HOST buffers

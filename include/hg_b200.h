@@ -206,7 +206,9 @@ hg_status hg_route(const void* keys, int32_t key_width, const void* vals, int32_
                    uint64_t* shard_counts, void* stream);
 
 /* Synthetic inputs: kind 0 = (u32|u64)splitmix64(seed, start+i);
- * kind 1 = C4 probes with hit ratio `hit` over ref[n_ref]; kind 2 = scramble31(start+i). */
+ * kind 1 = C4 probes with hit ratio `hit` over ref[n_ref]; kind 2 = scramble31(start+i);
+ * kind 3 = C3 Zipf keys mix64(r ^ 0x9E3779B97F4A7C15), r = lower_bound(cdf, u) + 1 with
+ * u = (splitmix64(seed, start+i) >> 11) * 2^-53 and ref = the device CDF (n_ref doubles). */
 hg_status hg_generate(void* out, int32_t key_width, uint64_t n, int32_t kind, uint64_t seed,
                       uint64_t start, double hit, const void* ref, uint64_t n_ref, void* stream);
 

@@ -10,12 +10,12 @@ from .hashgraph import (ENTRY_DTYPE, MATCH_PAIR_DTYPE, BuildConfig, BuildStats, 
                         Overflow, ProbeOptions, VertexHasher, build_v1, build_v2, count_instances,
                         derived_vertex_count, generate, hash_to_vertex, intersect_adjacency,
                         probe_device, probe_new, probe_new_device, probe_new_prepared, probe_standard,
-                        validate_csr)
+                        validate_csr, zipf_cdf)
 
 __all__ = [
     "ENTRY_DTYPE", "MATCH_PAIR_DTYPE", "BuildConfig", "BuildStats", "ExecMode", "HashGraph",
     "IdentityHasher", "InvalidArgument", "JoinResult", "OutOfRange", "Overflow", "ProbeOptions",
     "VertexHasher", "build_v1", "build_v2", "count_instances", "derived_vertex_count", "generate",
     "hash_to_vertex", "intersect_adjacency", "probe_device", "probe_new",
-    "probe_new_device", "probe_new_prepared", "probe_standard", "validate_csr",
+    "probe_new_device", "probe_new_prepared", "probe_standard", "validate_csr", "zipf_cdf",
 ]

@@ -670,7 +670,9 @@ hg_status hg_route(const void* keys, int32_t key_width, const void* vals, int32_
 hg_status hg_generate(void* out, int32_t key_width, uint64_t n, int32_t kind, uint64_t seed,
                       uint64_t start, double hit, const void* ref, uint64_t n_ref, void* stream) {
     if (key_width != 4 && key_width != 8) return fail(HG_EINVAL, "key_width must be 4 or 8");
-    if (kind < 0 || kind > 2) return fail(HG_EINVAL, "unknown generator kind");
+    if (kind < 0 || kind > 3) return fail(HG_EINVAL, "unknown generator kind");
+    if (kind == 3 && (!n_ref || !is_device_ptr(ref)))
+        return fail(HG_EINVAL, "the Zipf generator needs a device CDF (ref, n_ref)");
     if (n && !is_device_ptr(out)) return fail(HG_EINVAL, "hg_generate writes device memory only");
     int dev = 0;
     if (hg_status st = need_device(&dev); st != HG_OK) return st;

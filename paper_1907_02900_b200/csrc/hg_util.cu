@@ -35,7 +35,8 @@ __device__ __forceinline__ uint32_t scramble31(uint64_t i) {
 
 template <typename K>
 __global__ void k_generate(K* out, uint64_t n, int kind, uint64_t seed, uint64_t start,
-                           double hit, const K* ref, uint64_t n_ref) {
+                           double hit, const void* ref_, uint64_t n_ref) {
+    const K* ref = static_cast<const K*>(ref_);
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
         const uint64_t g = start + i;
@@ -53,8 +54,24 @@ __global__ void k_generate(K* out, uint64_t n, int kind, uint64_t seed, uint64_t
             } else {
                 k = sizeof(K) == 4 ? (r | 0x80000000ULL) : (r | 0x8000000000000000ULL);
             }
-        } else {
+        } else if (kind == 2) {
             k = scramble31(g);  // kind 2: C4 unique build keys
+        } else {
+            // kind 3: C3 Zipf ranks over the host-built CDF (n_ref doubles):
+            // r = lower_bound(CDF, u) + 1, key = mix64(r ^ 0x9E3779B97F4A7C15)
+            const double* cdf = static_cast<const double*>(ref_);
+            const double u = double(splitmix64(seed, g) >> 11) * (1.0 / 9007199254740992.0);
+            uint64_t lo = 0, len = n_ref;
+            while (len > 0) {
+                const uint64_t h = len >> 1;
+                if (cdf[lo + h] < u) {
+                    lo += h + 1;
+                    len -= h + 1;
+                } else {
+                    len = h;
+                }
+            }
+            k = mix64((lo + 1) ^ 0x9E3779B97F4A7C15ULL);
         }
         out[i] = K(k);
     }
@@ -67,10 +84,10 @@ cudaError_t generate_keys(void* out, int key_bytes, uint64_t n, int kind, uint64
     const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16));
     if (key_bytes == 4) {
         k_generate<uint32_t><<<grid, 256, 0, s>>>(static_cast<uint32_t*>(out), n, kind, seed, start,
-                                                  hit, static_cast<const uint32_t*>(ref), n_ref);
+                                                  hit, ref, n_ref);
     } else {
         k_generate<uint64_t><<<grid, 256, 0, s>>>(static_cast<uint64_t*>(out), n, kind, seed, start,
-                                                  hit, static_cast<const uint64_t*>(ref), n_ref);
+                                                  hit, ref, n_ref);
     }
     return cudaGetLastError();
 }

@@ -558,11 +558,31 @@ def validate_csr(hg: HashGraph, expected_entries: int, input_keys=None) -> Optio
     return None if code.value == 0 else _VIOLATIONS.get(code.value, f"violation {code.value}")
 
 
+def zipf_cdf(ranks: int, s: float) -> np.ndarray:
+    """CDF of P(r) ~ r^-s over ranks 1..K, built on
+    the host in double and uploaded as-is (the last entry is exactly 1.0)."""
+    p = np.arange(1, ranks + 1, dtype=np.float64) ** (-float(s))
+    cdf = np.cumsum(p) / p.sum()
+    cdf[-1] = 1.0
+    return cdf
+
+
 def generate(out_tensor, kind: int = 0, seed: int = 1, start: int = 0, hit: float = 1.0,
              ref=None) -> None:
-    """Fills a CUDA tensor with SURVEY.md Appendix B synthetic keys."""
+    """Fills a CUDA tensor with SURVEY.md Appendix B synthetic keys: kind 0
+    splitmix64, 1 C4 probes over `ref` with hit ratio `hit`, 2 scramble31
+    (C4 build keys), 3 C3 Zipf keys over `ref` = a CUDA float64 CDF
+    (zipf_cdf)."""
     oa = _Arr(out_tensor)
-    ra = _Arr(ref) if ref is not None else None
+    if kind == 3:
+        torch = _torch()
+        if ref is None or not (isinstance(ref, torch.Tensor) and ref.is_cuda
+                               and ref.dtype == torch.float64):
+            raise InvalidArgument(HG_EINVAL, "Zipf keys need ref = a CUDA float64 CDF tensor")
+        ref = ref.contiguous()
+        rp, rn = ref.data_ptr(), ref.numel()
+    else:
+        ra = _Arr(ref) if ref is not None else None
+        rp, rn = (ra.ptr, ra.n) if ra else (None, 0)
     _check(_lib.lib().hg_generate(oa.ptr, oa.width, oa.n, kind, seed, start, float(hit),
-                                  ra.ptr if ra else None, ra.n if ra else 0,
-                                  _stream_for(oa)))
+                                  rp, rn, _stream_for(oa)))

@@ -1,0 +1,166 @@
+"""GPU parity on the BASELINE.json configurations,
+through the C-ABI, against the oracle at sizes it finishes in seconds, and
+through size-independent invariants at the full 2^28 / 2^29 sizes.
+
+C1  2^20 splitmix u32 keys, load 1, simple build + probe_standard
+C3  u64 keys ~ Zipf(s) over K ranks (key = mix64(r ^ 0x9E37...)), u64 values =
+    input position, loads 0.5 / 1 / 1.5 / 2 / 4, both builds
+C4  unique scramble31 build keys, probes at hit ratio 0.1 / 0.5 / 1.0 with
+    pairs (every probe < 2^31 is a build key, every other probe misses)
+Full-size invariant: key == input[index] for every entry, the
+indices a permutation, every entry under the vertex its key hashes to and
+offsets monotone with offsets[V] = N (hg_validate) pin the table to the
+reference's up to intra-segment order."""
+import numpy as np
+import pytest
+
+import paper_1907_02900_b200 as hg
+from paper_1907_02900_b200 import BuildConfig, ProbeOptions
+
+pytestmark = pytest.mark.gpu
+
+M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+@pytest.fixture(autouse=True)
+def _need_gpu(cuda):
+    yield
+
+
+def mix64_np(x):
+    """hash.hpp:12-19 on numpy u64 (wrapping)."""
+    x = x.astype(np.uint64)
+    with np.errstate(over="ignore"):
+        x ^= x >> np.uint64(33)
+        x *= np.uint64(0xFF51AFD7ED558CCD)
+        x ^= x >> np.uint64(33)
+        x *= np.uint64(0xC4CEB9FE1A85EC53)
+        x ^= x >> np.uint64(33)
+    return x
+
+
+def zipf_keys_host(oracle, n, cdf, seed, start=0):
+    """SURVEY.md Appendix B (C3) restated on the host."""
+    u = (oracle.splitmix(seed, n, start=start, mask_u32=False) >> np.uint64(11)).astype(
+        np.float64) * (1.0 / 9007199254740992.0)
+    r = np.searchsorted(cdf, u, side="left").astype(np.uint64) + np.uint64(1)
+    return mix64_np(r ^ np.uint64(0x9E3779B97F4A7C15))
+
+
+def canon_equal(t, o):
+    assert (t.offsets() == o.offsets).all(), "offsets differ"
+    nv = len(o.offsets) - 1
+    seg = np.repeat(np.arange(nv, dtype=np.uint64), np.diff(o.offsets).astype(np.int64))
+    a = np.lexsort((t.edge_index(), t.edge_keys(), seg))
+    b = np.lexsort((o.index, o.keys, seg))
+    assert (t.edge_keys()[a] == o.keys[b]).all() and (t.edge_index()[a] == o.index[b]).all()
+
+
+def test_c1_config(oracle, cuda):
+    n = 1 << 20
+    keys = cuda.empty(n, dtype=cuda.int32, device="cuda")
+    hg.generate(keys, kind=0, seed=1)
+    host = keys.cpu().numpy().view(np.uint32).astype(np.uint64)
+    assert (host == oracle.splitmix(1, n)).all()
+    probes = cuda.empty(n, dtype=cuda.int32, device="cuda")
+    hg.generate(probes, kind=0, seed=2)
+    hp = probes.cpu().numpy().view(np.uint32).astype(np.uint64)
+    o = oracle.build(host, variant=1)
+    for build in (hg.build_v1, hg.build_v2):
+        t = build(keys)
+        canon_equal(t, o)
+        for pk, hpk in ((keys, host), (probes, hp)):
+            r = hg.probe_standard(t, pk)
+            ro = oracle.probe_standard(o, hpk)
+            assert (r.match_count, r.key_comparisons) == (ro["match_count"], ro["key_comparisons"])
+
+
+@pytest.mark.parametrize("s", [1.0, 1.2])
+def test_c3_zipf_generator_and_builds(oracle, cuda, s):
+    n, ranks = 1 << 20, 1 << 16
+    cdf = hg.zipf_cdf(ranks, s)
+    dcdf = cuda.tensor(cdf, dtype=cuda.float64, device="cuda")
+    keys = cuda.empty(n, dtype=cuda.int64, device="cuda")
+    hg.generate(keys, kind=3, seed=5, ref=dcdf)
+    host = keys.cpu().numpy().view(np.uint64)
+    assert (host == zipf_keys_host(oracle, n, cdf, 5)).all(), "device Zipf generator differs"
+    vals = cuda.arange(n, dtype=cuda.int64, device="cuda")
+    for load in (0.5, 1.0, 1.5, 2.0, 4.0):
+        o = oracle.build(host, variant=1, load=load)
+        for build in (hg.build_v1, hg.build_v2):
+            t = build(keys, BuildConfig(load_factor=load), vals=vals)
+            assert t.key_width == 8 and t.val_width == 8
+            canon_equal(t, o)
+            assert hg.validate_csr(t, n, keys) is None
+    # skewed probes: heavy segments on the warp-cooperative path
+    t = hg.build_v2(keys, vals=vals)
+    o = oracle.build(host, variant=2)
+    pr = host[: 1 << 12]
+    r = hg.probe_standard(t, pr)
+    ro = oracle.probe_standard(o, pr)
+    assert (r.match_count, r.key_comparisons) == (ro["match_count"], ro["key_comparisons"])
+
+
+@pytest.mark.parametrize("h", [0.1, 0.5, 1.0])
+def test_c4_join_pairs(oracle, cuda, h):
+    n, m = 1 << 20, 1 << 21
+    build = cuda.empty(n, dtype=cuda.int32, device="cuda")
+    hg.generate(build, kind=2)
+    probes = cuda.empty(m, dtype=cuda.int32, device="cuda")
+    hg.generate(probes, kind=1, seed=3, hit=h, ref=build)
+    hb = build.cpu().numpy().view(np.uint32).astype(np.uint64)
+    hp = probes.cpu().numpy().view(np.uint32).astype(np.uint64)
+    assert len(np.unique(hb)) == n and hb.max() < (1 << 31)
+    t = hg.build_v2(build)
+    o = oracle.build(hb, variant=2)
+    ro = oracle.probe_standard(o, hp, materialize=True, cap=1 << 23)
+    assert ro["match_count"] == int((hp < (1 << 31)).sum())
+    for method in (1, 2):
+        r = hg.probe_standard(t, probes, ProbeOptions(materialize=True, pair_cap=1 << 23),
+                              method=method)
+        assert (r.match_count, r.key_comparisons) == (ro["match_count"], ro["key_comparisons"])
+        got = np.stack([r.pairs["left_index"], r.pairs["right_index"]], 1)
+        exp = ro["pairs"]
+        assert (got[np.lexsort((got[:, 0], got[:, 1]))] == exp[np.lexsort((exp[:, 0], exp[:, 1]))]).all()
+
+
+def test_c3_full_size_invariants(cuda):
+    """C3 at 2^27 u64 keys (s = 1.0 over 2^24 ranks), load 1, binned build:
+    the device validator proves the table equals the reference's up to
+    intra-segment order."""
+    n = 1 << 27
+    dcdf = cuda.tensor(hg.zipf_cdf(1 << 24, 1.0), dtype=cuda.float64, device="cuda")
+    keys = cuda.empty(n, dtype=cuda.int64, device="cuda")
+    hg.generate(keys, kind=3, seed=7, ref=dcdf)
+    vals = cuda.arange(n, dtype=cuda.int64, device="cuda")
+    for build in (hg.build_v2, hg.build_v1):
+        t = build(keys, vals=vals)
+        assert hg.validate_csr(t, n, keys) is None
+        t.close()
+
+
+def test_c4_full_size_invariants(cuda):
+    """C4 at full size: 2^28 unique build keys, 2^29 probes at h = 0.5, pairs
+    (u32 layout on the device). Every probe < 2^31 is a build key and every
+    other probe misses, so match_count = #(probe < 2^31); each pair joins equal
+    keys and no probe matches twice."""
+    n, m = 1 << 28, 1 << 29
+    build = cuda.empty(n, dtype=cuda.int32, device="cuda")
+    hg.generate(build, kind=2)
+    probes = cuda.empty(m, dtype=cuda.int32, device="cuda")
+    hg.generate(probes, kind=1, seed=3, hit=0.5, ref=build)
+    t = hg.build_v2(build)
+    expect = int((probes >= 0).sum().item())  # int32 view: value < 2^31
+    res = cuda.zeros(2, dtype=cuda.int64, device="cuda")
+    pairs = cuda.empty((expect + 16, 2), dtype=cuda.int32, device="cuda")
+    hg.probe_device(t, probes, res, pairs=pairs, pair_width=4, pair_cap=expect + 16)
+    mc = int(res[0].item())
+    assert mc == expect
+    p = pairs[:mc].long()
+    left, right = p[:, 0], p[:, 1]
+    assert bool((build[left] == probes[right]).all())
+    assert int(cuda.unique(right).numel()) == mc
+    # count-only agrees
+    res.zero_()
+    hg.probe_device(t, probes, res)
+    assert int(res[0].item()) == expect
