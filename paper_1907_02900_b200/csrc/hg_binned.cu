@@ -60,7 +60,7 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
              const OffT* __restrict__ part_start /* nparts + 1 partition offsets */,
              uint64_t nparts, uint64_t nv_total, uint64_t seed, int hk, Divisor nv,
              uint32_t pshift, OffT* __restrict__ offs, K* __restrict__ okeys,
-             VT* __restrict__ ovals) {
+             VT* __restrict__ ovals, uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_n) {
     using PE = EntryT<K, VT>;
     using E = typename PE::T;
     using L = BuildLayout<K, VT>;
@@ -147,10 +147,13 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
                 }
             }
         } else {
-            for (uint32_t i = tid; i < cntp; i += kBuildBlock) {
-                const uint32_t lv = uint32_t(hv<POW2>(PE::key(reorg[s + i]), seed, hk, nv) - vb);
-                atomicAdd(cnt + lv, 1u);
-            }
+            // oversized (skewed) partition: built by the grid-wide K7b
+            // kernels; here only its counters (offs[vb+1 .. vb+pv]) are zeroed
+            for (uint32_t j = tid; j < pv; j += kBuildBlock) offs[vb + j + 1] = OffT(0);
+            if (p == 0 && tid == 0) offs[0] = 0;
+            if (tid == 0) big_list[atomicAdd(big_n, 1u)] = uint32_t(p);
+            __syncthreads();
+            continue;
         }
         __syncthreads();
         // exclusive scan of cnt[0..pv): thread owns `per` consecutive counters
@@ -236,18 +239,125 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
             const bool a = bulk_store_span(okeys + s, skp, cntp, tid, kBuildBlock);
             const bool b = bulk_store_span(ovals + s, svp, cntp, tid, kBuildBlock);
             if (a || b) bulk_commit();
-        } else {
-            for (uint32_t i = tid; i < cntp; i += kBuildBlock) {
-                const E en = reorg[s + i];
-                const uint32_t lv = uint32_t(hv<POW2>(PE::key(en), seed, hk, nv) - vb);
-                const uint64_t pos = s + atomicAdd(cnt + lv, 1u);
-                okeys[pos] = PE::key(en);
-                ovals[pos] = PE::val(en);
-            }
         }
         __syncthreads();
     }
     if (tid == 0) bulk_wait_all();
+}
+
+// ---------------------------------------------------------------- K7b
+// Partitions holding more entries than K7 can stage (heavy keys under skew,
+// e.g. C3's Zipf ranks) are built by the whole grid instead of one CTA, with
+// the partition's slice of `offs` as counter / cursor array (the V1 scheme):
+//   k7b_prefix  one thread: prefix of the queued partitions' entry counts
+//   k7b_count   grid-stride over all queued entries; warp-aggregated global
+//               atomics on offs[v+1] (a hot vertex costs one atomic per warp)
+//   k7b_scan    one CTA per queued partition: offs[v+1] := s + exclusive
+//               prefix (the placement cursor)
+//   k7b_place   grid-stride again; aggregated tickets on the cursors leave
+//               offs[v+1] = end(v) and give each entry its slot
+template <typename OffT>
+__global__ void k7b_prefix(const OffT* __restrict__ part_start, const uint32_t* __restrict__ list,
+                           const uint32_t* __restrict__ big_n, uint64_t* __restrict__ pref) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const uint32_t nb = *big_n;
+    uint64_t acc = 0;
+    for (uint32_t i = 0; i < nb; ++i) {
+        pref[i] = acc;
+        acc += uint64_t(part_start[list[i] + 1]) - uint64_t(part_start[list[i]]);
+    }
+    pref[nb] = acc;
+}
+
+// Queued entry g -> (partition index in the list, entry position).
+__device__ __forceinline__ uint32_t big_owner(const uint64_t* pref, uint32_t nb, uint64_t g) {
+    uint32_t lo = 0, hi = nb;  // pref[lo] <= g < pref[hi]
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (pref[mid] <= g) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+template <typename K, typename VT, typename OffT, int POW2, bool PLACE>
+__global__ void __launch_bounds__(256)
+k7b_pass(const typename EntryT<K, VT>::T* __restrict__ reorg, const OffT* __restrict__ part_start,
+         const uint32_t* __restrict__ list, const uint32_t* __restrict__ big_n,
+         const uint64_t* __restrict__ pref, uint64_t seed, Divisor nv, uint32_t pshift,
+         OffT* __restrict__ offs, K* __restrict__ okeys, VT* __restrict__ ovals) {
+    using PE = EntryT<K, VT>;
+    constexpr bool V32 = sizeof(OffT) == 4;
+    const uint32_t nb = *big_n;
+    if (nb == 0) return;
+    const uint64_t total = pref[nb];
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t g0 = uint64_t(blockIdx.x) * blockDim.x; g0 < total; g0 += stride) {
+        const uint64_t g = g0 + threadIdx.x;
+        const bool act = g < total;
+        const uint32_t active = __ballot_sync(0xffffffffu, act);
+        if (!act) continue;
+        const uint32_t li = big_owner(pref, nb, g);
+        const uint64_t p = list[li];
+        const uint64_t pos = uint64_t(part_start[p]) + (g - pref[li]);
+        const auto en = reorg[pos];
+        const uint64_t v = vhash<POW2>(PE::key(en), seed, nv);  // local vertex id
+        if constexpr (!PLACE) {
+            aggregated_count<V32>(offs + v + 1, active, v);
+        } else {
+            const uint64_t slot = aggregated_ticket<V32>(offs + v + 1, active, v);
+            okeys[slot] = PE::key(en);
+            ovals[slot] = PE::val(en);
+        }
+    }
+    (void)pshift;
+}
+
+template <typename OffT>
+__global__ void __launch_bounds__(1024)
+k7b_scan(const OffT* __restrict__ part_start, const uint32_t* __restrict__ list,
+         const uint32_t* __restrict__ big_n, uint64_t nv_total, uint32_t pshift,
+         OffT* __restrict__ offs) {
+    __shared__ uint64_t s_warp[32];
+    __shared__ uint64_t s_carry, s_tot;
+    const uint32_t nb = *big_n;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t li = blockIdx.x; li < nb; li += gridDim.x) {
+        const uint64_t p = list[li];
+        const uint64_t vb = p << pshift;
+        const uint64_t P = uint64_t(1) << pshift;
+        const uint64_t pv = nv_total - vb < P ? nv_total - vb : P;
+        if (threadIdx.x == 0) s_carry = part_start[p];
+        __syncthreads();
+        for (uint64_t j0 = 0; j0 < pv; j0 += blockDim.x) {
+            const uint64_t j = j0 + threadIdx.x;
+            const uint64_t c = j < pv ? uint64_t(offs[vb + j + 1]) : 0;
+            uint64_t inc = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint64_t y = __shfl_up_sync(0xffffffffu, inc, d);
+                if (int(lane) >= d) inc += y;
+            }
+            if (lane == 31) s_warp[warp] = inc;
+            __syncthreads();
+            if (warp == 0) {
+                const uint64_t w = lane < (blockDim.x >> 5) ? s_warp[lane] : 0;
+                uint64_t wi = w;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint64_t y = __shfl_up_sync(0xffffffffu, wi, d);
+                    if (int(lane) >= d) wi += y;
+                }
+                if (lane < (blockDim.x >> 5)) s_warp[lane] = wi - w;
+                if (lane == 31) s_tot = wi;  // chunk total
+            }
+            __syncthreads();
+            const uint64_t carry = s_carry;
+            if (j < pv) offs[vb + j + 1] = OffT(carry + s_warp[warp] + inc - c);
+            __syncthreads();
+            if (threadIdx.x == 0) s_carry = carry + s_tot;
+            __syncthreads();
+        }
+    }
 }
 
 template <typename K, typename VT, typename OffT, int POW2>
@@ -271,16 +381,23 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
     const size_t ps_bytes = ((g.nparts + 1) * sizeof(OffT) + 255) & ~size_t(255);
     const size_t pscr = PartitionScratch<K, VT, OffT>::bytes(g, t.n);
     const size_t reorg_bytes = (t.n * sizeof(E) + 255) & ~size_t(255);
+    // K7b queue: at most nparts oversized partitions
+    const size_t list_bytes = ((g.nparts + 1) * 4 + 255) & ~size_t(255);
+    const size_t pref_bytes = ((g.nparts + 1) * 8 + 255) & ~size_t(255);
     char* scratch = nullptr;
     if ((e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
-                             ps_bytes + pscr + reorg_bytes + 256, s)) != cudaSuccess)
+                             ps_bytes + pscr + reorg_bytes + list_bytes + pref_bytes + 256, s)) !=
+        cudaSuccess)
         return e;
     OffT* part_start = reinterpret_cast<OffT*>(scratch);
     void* pscratch = scratch + ps_bytes;
     E* reorg = reinterpret_cast<E*>(scratch + ps_bytes + pscr);
-    uint32_t* ticket = reinterpret_cast<uint32_t*>(scratch + ps_bytes + pscr + reorg_bytes);
+    uint32_t* big_list = reinterpret_cast<uint32_t*>(scratch + ps_bytes + pscr + reorg_bytes);
+    uint64_t* big_pref = reinterpret_cast<uint64_t*>(scratch + ps_bytes + pscr + reorg_bytes + list_bytes);
+    uint32_t* ticket = reinterpret_cast<uint32_t*>(scratch + ps_bytes + pscr + reorg_bytes + list_bytes +
+                                                   pref_bytes);
     do {
-        if ((e = cudaMemsetAsync(ticket, 0, 4, s)) != cudaSuccess) break;
+        if ((e = cudaMemsetAsync(ticket, 0, 8, s)) != cudaSuccess) break;  // ticket + big_n
         e = partition<K, VT, OffT, POW2>(static_cast<const K*>(a.keys),
                                          static_cast<const VT*>(a.vals), t.n, t.seed, t.hash_kind,
                                          nv, g, part_start, pscratch, reorg, s, kBuildPassNames);
@@ -297,7 +414,26 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
                   kb<<<gk, kBuildBlock, smem, s>>>(reorg, part_start, g.nparts, t.nv, t.seed,
                                                    t.hash_kind, nv, g.pshift, offs,
                                                    static_cast<K*>(t.keys),
-                                                   static_cast<VT*>(t.vals)));
+                                                   static_cast<VT*>(t.vals), big_list,
+                                                   ticket + 1));
+        if ((e = cudaGetLastError()) != cudaSuccess) break;
+        // oversized partitions (device-side count; the kernels exit at once
+        // when there are none)
+        uint32_t* big_n = ticket + 1;
+        k7b_prefix<OffT><<<1, 32, 0, s>>>(part_start, big_list, big_n, big_pref);
+        const unsigned gb = unsigned(num_sms() * 8);
+        HG_LAUNCH("k7b_big_count", s,
+                  (k7b_pass<K, VT, OffT, POW2, false><<<gb, 256, 0, s>>>(
+                      reorg, part_start, big_list, big_n, big_pref, t.seed, nv, g.pshift, offs,
+                      nullptr, nullptr)));
+        HG_LAUNCH("k7b_big_scan", s,
+                  (k7b_scan<OffT><<<unsigned(num_sms() * 2), 1024, 0, s>>>(part_start, big_list,
+                                                                       big_n, t.nv, g.pshift,
+                                                                       offs)));
+        HG_LAUNCH("k7b_big_place", s,
+                  (k7b_pass<K, VT, OffT, POW2, true><<<gb, 256, 0, s>>>(
+                      reorg, part_start, big_list, big_n, big_pref, t.seed, nv, g.pshift, offs,
+                      static_cast<K*>(t.keys), static_cast<VT*>(t.vals))));
         e = cudaGetLastError();
     } while (false);
     cudaFreeAsync(scratch, s);

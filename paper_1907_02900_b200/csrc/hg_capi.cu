@@ -438,6 +438,7 @@ hg_status hg_probe(const hg_table* t, const void* probes, int32_t probe_width, u
     a.probes = dprobes;
     a.m = m;
     a.counts = counts;
+    a.counts_requested = opts.counts != nullptr;
     a.totals = totals;
     a.pairs = pairs;
     a.pair_bytes = opts.pair_width;

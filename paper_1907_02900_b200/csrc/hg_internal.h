@@ -43,7 +43,9 @@ cudaError_t build_table(const TableDesc& t, const BuildArgs& a, cudaStream_t s);
 struct ProbeArgs {
     const void* probes = nullptr;  // device, m entries of key_bytes (same as table)
     uint64_t m = 0;
-    uint32_t* counts = nullptr;    // nullable: per-probe match counts (u32)
+    uint32_t* counts = nullptr;    // nullable: per-probe match counts (u32); scratch for the
+                                   // direct pairs path when the caller did not ask for counts
+    bool counts_requested = true;  // the caller wants `counts` filled (in probe order)
     uint64_t* totals = nullptr;    // device [2]: match_count, key_comparisons (accumulated)
     // pairs (K9/K10): when pairs != nullptr, pair_offsets must hold m+1 u64.
     void* pairs = nullptr;         // device, cap pairs of pair_bytes*2

@@ -434,7 +434,8 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
     const double pmean = double(a.m) * double(P) / double(t.nv);
     const uint32_t kcap = uint32_t(std::min(12288.0, std::max(512.0, 1.5 * kmean + 256)));
     const uint32_t pcap = uint32_t(std::min(12288.0, std::max(512.0, 1.5 * pmean + 256)));
-    const bool need_idx = a.counts != nullptr || a.pairs != nullptr;
+    const bool want_counts = a.counts != nullptr && a.counts_requested;
+    const bool need_idx = want_counts || a.pairs != nullptr;
     const int sms = num_sms();
     cudaError_t e;
     char* scratch = nullptr;
@@ -525,7 +526,7 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
         e = launch(k_probe_part<K, VT, OffT, IT, POW2, 1, false, uint32_t>, "k8p_probe_part",
                    pcount, nullptr, nullptr, 0);
         if (e != cudaSuccess) break;
-        if (a.counts) {
+        if (want_counts) {
             HG_LAUNCH("p_counts_scatter", s,
                       (k_scatter_counts<K, IT><<<unsigned(std::min<uint64_t>((a.m + 255) / 256,
                                                                              uint64_t(sms) * 16)),
