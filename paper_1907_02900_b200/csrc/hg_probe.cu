@@ -409,6 +409,292 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
     }
 }
 
+// ------------------------------------------------ single-pass pairs (K10p)
+// Pairs without per-probe count arrays or a global scan: partitions are taken
+// in ticket order; per partition (staged in shared memory as in
+// k_probe_part) the CTA
+//   A  counts the matches of every probe, keeping per-(chunk, warp) totals
+//      (chunk = 512 consecutive probes) for the first kPairRound chunks,
+//   -  publishes the partition total with a decoupled look-back over
+//      partitions (hg_scan.cuh status words) -> the partition's first slot,
+//   B  scans the (chunk, warp) totals and writes every probe's pairs at
+//      slot = base + (chunk, warp) prefix + warp-exclusive count.
+// HBM traffic = the count-only probe's + the pairs themselves. Pair order:
+// partition, then probe within the partition, then table segment order (the
+// reference's order is unspecified too, join.hpp:71-74).
+constexpr uint32_t kPairRound = 24;  // chunks per scan round (24 * 512 = 12288 probes)
+
+// Per-lane match count of probe `i` of the partition (valid < qn), with
+// warp-cooperative walks of long segments; warp-collective.
+template <typename K, typename OffT, typename PEnt, typename PE, int POW2>
+__device__ __forceinline__ uint32_t pair_count(const K* __restrict__ kp, const PEnt& ent,
+                                               const OffT* soff, uint64_t i, uint64_t qn, uint64_t tb,
+                                               uint64_t vb, uint64_t seed, int hk, const Divisor& nv,
+                                               uint64_t& compared, K& key, uint64_t& b, uint64_t& e) {
+    const uint32_t lane = threadIdx.x & 31;
+    b = e = 0;
+    key = 0;
+    if (i < qn) {
+        key = PE::key(ent);
+        const uint32_t lv = uint32_t(hv<POW2>(key, seed, hk, nv) - vb);
+        b = uint64_t(soff[lv]) - tb;
+        e = uint64_t(soff[lv + 1]) - tb;
+    }
+    const uint64_t len = e - b;
+    compared += len;
+    uint32_t c = 0;
+    if (len <= kLongSeg)
+        for (uint64_t t = b; t < e; ++t) c += kp[t] == key;
+    uint32_t longm = __ballot_sync(0xffffffffu, len > kLongSeg);
+    while (longm) {
+        const int src = __ffs(longm) - 1;
+        longm &= longm - 1;
+        const uint64_t kb = __shfl_sync(0xffffffffu, b, src);
+        const uint64_t ke = __shfl_sync(0xffffffffu, e, src);
+        const K kk = __shfl_sync(0xffffffffu, key, src);
+        uint32_t cc = 0;
+        for (uint64_t t = kb + lane; t < ke; t += 32) cc += kp[t] == kk;
+        cc = warp_sum(cc);
+        if (int(lane) == src) c = cc;
+    }
+    return c;
+}
+
+template <typename K, typename VT, typename OffT, typename IT, int POW2, typename PT>
+__global__ void __launch_bounds__(kPartProbeBlock)
+k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __restrict__ ppart,
+              uint64_t nparts, uint64_t nv_total, uint64_t seed, int hk, Divisor nv,
+              uint32_t pshift, const OffT* __restrict__ offs, const K* __restrict__ tkeys,
+              const VT* __restrict__ tvals, uint32_t kcap, uint32_t pcap, uint64_t* __restrict__ status,
+              void* __restrict__ pairs, uint64_t cap, uint64_t* __restrict__ totals,
+              uint32_t* ticket) {
+    using PE = EntryT<K, IT>;
+    using PEnt = typename PE::T;
+    using L = ProbeLayout<K, OffT, PEnt>;
+    constexpr uint32_t nwarps = kPartProbeBlock / 32;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const uint32_t P = 1u << pshift;
+    unsigned char* const b_off = smem;
+    unsigned char* const b_key = smem + L::off_bytes(P);
+    unsigned char* const b_ent = b_key + L::key_bytes(kcap);
+    __shared__ uint64_t s_bar;
+    __shared__ uint64_t s_p, s_tb, s_q0, s_q1, s_base;
+    __shared__ uint32_t s_o0, s_o1, s_o2, s_kst, s_pst;
+    __shared__ uint64_t s_wt[kPairRound * nwarps];
+    __shared__ uint64_t s_red[nwarps];
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        mbar_init(&s_bar, 1);
+        fence_mbar_init();
+    }
+    uint32_t phase = 0;
+    uint64_t matches = 0, compared = 0;
+    while (true) {
+        if (tid == 0) {
+            const uint64_t p = atomicAdd(ticket, 1u);
+            s_p = p;
+            if (p < nparts) {
+                const uint64_t vb = p << pshift;
+                const uint32_t pv = uint32_t(nv_total - vb < P ? nv_total - vb : uint64_t(P));
+                const uint64_t tb = offs[vb], te = offs[vb + pv];
+                const uint64_t q0 = ppart[p], q1 = ppart[p + 1];
+                s_tb = tb;
+                s_q0 = q0;
+                s_q1 = q1;
+                s_kst = te - tb <= kcap;
+                s_pst = pcap && q1 - q0 <= pcap;
+                fence_proxy_async();
+                const uintptr_t ao = reinterpret_cast<uintptr_t>(offs + vb);
+                const uintptr_t ak = reinterpret_cast<uintptr_t>(tkeys + tb);
+                const uintptr_t ae = reinterpret_cast<uintptr_t>(pin + q0);
+                auto span = [](uintptr_t a, size_t bytes, uint32_t& lo_off) -> uint32_t {
+                    const uintptr_t lo = a & ~uintptr_t(15), hi = (a + bytes + 15) & ~uintptr_t(15);
+                    lo_off = uint32_t(a - lo);
+                    return uint32_t(hi - lo);
+                };
+                uint32_t o0, o1 = 0, o2 = 0;
+                const uint32_t l0 = span(ao, size_t(pv + 1) * sizeof(OffT), o0);
+                const uint32_t l1 = s_kst ? span(ak, size_t(te - tb) * sizeof(K), o1) : 0;
+                const uint32_t l2 = s_pst ? span(ae, size_t(q1 - q0) * sizeof(PEnt), o2) : 0;
+                s_o0 = o0;
+                s_o1 = o1;
+                s_o2 = o2;
+                mbar_arrive_expect_tx(&s_bar, l0 + l1 + l2);
+                tma_load_1d(b_off, reinterpret_cast<const void*>(ao - o0), l0, &s_bar);
+                if (l1) tma_load_1d(b_key, reinterpret_cast<const void*>(ak - o1), l1, &s_bar);
+                if (l2) tma_load_1d(b_ent, reinterpret_cast<const void*>(ae - o2), l2, &s_bar);
+            }
+        }
+        __syncthreads();
+        const uint64_t p = s_p;
+        if (p >= nparts) break;
+        const uint64_t vb = p << pshift;
+        const uint64_t tb = s_tb;
+        const uint64_t q0 = s_q0, qn = s_q1 - s_q0;
+        const OffT* soff = reinterpret_cast<const OffT*>(b_off + s_o0);
+        mbar_wait(&s_bar, phase);
+        phase ^= 1;
+        const uint64_t nchunks = (qn + kPartProbeBlock - 1) / kPartProbeBlock;
+        auto run = [&](const K* __restrict__ kp, const PEnt* __restrict__ ep) {
+            // A: counts; (chunk, warp) totals of the first round
+            uint64_t mine = 0;
+            const uint64_t i0 = warp * 32 + lane;
+            PEnt nxt = i0 < qn ? ep[i0] : PEnt{};
+            for (uint64_t ch = 0; ch < nchunks; ++ch) {
+                K key;
+                uint64_t b, e;
+                const uint64_t i = ch * kPartProbeBlock + i0;
+                const PEnt cur = nxt;  // entries are prefetched one chunk ahead
+                if (i + kPartProbeBlock < qn) nxt = ep[i + kPartProbeBlock];
+                const uint32_t c = pair_count<K, OffT, PEnt, PE, POW2>(kp, cur, soff, i, qn, tb, vb, seed,
+                                                                        hk, nv, compared, key, b, e);
+                const uint32_t cw = warp_sum(c);
+                if (ch < kPairRound && lane == 0) s_wt[ch * nwarps + warp] = cw;
+                mine += cw;
+            }
+            if (lane == 0) s_red[warp] = mine;
+            __syncthreads();
+            if (warp == 0) {
+                uint64_t tot = lane < nwarps ? s_red[lane] : 0;
+                tot = warp_sum(tot);
+                uint64_t prefix = 0;
+                if (p == 0) {
+                    if (lane == 0) st_relaxed_u64(status, kScanFlagIncl | tot);
+                } else {
+                    if (lane == 0) st_relaxed_u64(status + p, kScanFlagAgg | tot);
+                    int64_t idx = int64_t(p) - 1;
+                    while (true) {
+                        const int64_t jj = idx - int64_t(lane);
+                        uint64_t sw = kScanFlagIncl;
+                        if (jj >= 0) {
+                            do {
+                                sw = ld_relaxed_u64(status + jj);
+                            } while ((sw >> 62) == 0);
+                        }
+                        const uint32_t inclm = __ballot_sync(0xffffffffu, (sw >> 62) == 2);
+                        const uint32_t stop = inclm ? uint32_t(__ffs(inclm) - 1) : 32u;
+                        prefix += warp_sum(lane <= stop ? (sw & kScanValMask) : uint64_t(0));
+                        if (inclm) break;
+                        idx -= 32;
+                    }
+                    if (lane == 0) st_relaxed_u64(status + p, kScanFlagIncl | (prefix + tot));
+                }
+                if (lane == 0) {
+                    s_base = prefix;
+                    matches += tot;
+                }
+            }
+            __syncthreads();
+            uint64_t base = s_base;
+            // B: rounds of kPairRound chunks
+            for (uint64_t r0 = 0; r0 < nchunks && base < cap; r0 += kPairRound) {
+                const uint64_t r1 = r0 + kPairRound < nchunks ? r0 + kPairRound : nchunks;
+                if (r0 > 0) {
+                    __syncthreads();
+                    for (uint64_t ch = r0; ch < r1; ++ch) {
+                        K key;
+                        uint64_t b, e, dummy = 0;
+                        const uint64_t i = ch * kPartProbeBlock + warp * 32 + lane;
+                        const PEnt cur = i < qn ? ep[i] : PEnt{};
+                        const uint32_t c = pair_count<K, OffT, PEnt, PE, POW2>(
+                            kp, cur, soff, i, qn, tb, vb, seed, hk, nv, dummy, key, b, e);
+                        const uint32_t cw = warp_sum(c);
+                        if (lane == 0) s_wt[(ch - r0) * nwarps + warp] = cw;
+                    }
+                }
+                __syncthreads();
+                if (warp == 0) {
+                    // exclusive scan of (r1 - r0) * nwarps totals in (chunk, warp) order
+                    constexpr uint32_t per = kPairRound * nwarps / 32;
+                    uint64_t x[per];
+                    uint64_t sum = 0;
+#pragma unroll
+                    for (uint32_t k = 0; k < per; ++k) sum += (x[k] = s_wt[lane * per + k]);
+                    const uint64_t inc = warp_inclusive_sum(sum);
+                    uint64_t run_ = inc - sum;
+#pragma unroll
+                    for (uint32_t k = 0; k < per; ++k) {
+                        s_wt[lane * per + k] = run_;  // relative to the round's base
+                        run_ += x[k];
+                    }
+                    if (lane == 31) s_red[0] = inc;  // round total
+                }
+                __syncthreads();
+                const uint64_t round_total = s_red[0];
+                const uint64_t ib = r0 * kPartProbeBlock + warp * 32 + lane;
+                PEnt nxtb = ib < qn ? ep[ib] : PEnt{};
+                for (uint64_t ch = r0; ch < r1; ++ch) {
+                    K key;
+                    uint64_t b, e, dummy = 0;
+                    const uint64_t i = ch * kPartProbeBlock + warp * 32 + lane;
+                    const PEnt cur = nxtb;
+                    if (ch + 1 < r1 && i + kPartProbeBlock < qn) nxtb = ep[i + kPartProbeBlock];
+                    const uint32_t c = pair_count<K, OffT, PEnt, PE, POW2>(
+                        kp, cur, soff, i, qn, tb, vb, seed, hk, nv, dummy, key, b, e);
+                    const uint32_t incl = warp_inclusive_sum(c);
+                    uint64_t sl = base + s_wt[(ch - r0) * nwarps + warp] + (incl - c);
+                    const uint64_t len = e - b;
+                    const uint64_t pidx = PE::kHasVal && i < qn ? uint64_t(PE::val(cur)) : 0;
+                    if (c == 1 && len <= kLongSeg) {
+                        // common case (unique build keys): locate the hit in shared
+                        // memory first, so the value gather and the store are one
+                        // round trip for the whole warp instead of one per step
+                        uint64_t th = b;
+                        for (uint64_t t = b; t < e; ++t)
+                            if (kp[t] == key) th = t;
+                        if (sl < cap) store_pair<PT>(pairs, sl, uint64_t(tvals[tb + th]), pidx);
+                    } else if (c && len <= kLongSeg) {
+                        for (uint64_t t = b; t < e && sl < cap; ++t) {
+                            if (kp[t] == key) {
+                                store_pair<PT>(pairs, sl, uint64_t(tvals[tb + t]), pidx);
+                                ++sl;
+                            }
+                        }
+                    }
+                    uint32_t lm = __ballot_sync(0xffffffffu, c && len > kLongSeg);
+                    while (lm) {
+                        const int src = __ffs(lm) - 1;
+                        lm &= lm - 1;
+                        const uint64_t kb = __shfl_sync(0xffffffffu, b, src);
+                        const uint64_t ke = __shfl_sync(0xffffffffu, e, src);
+                        const K kk = __shfl_sync(0xffffffffu, key, src);
+                        uint64_t ws = __shfl_sync(0xffffffffu, sl, src);
+                        const uint64_t pj = __shfl_sync(0xffffffffu, pidx, src);
+                        for (uint64_t t0 = kb; t0 < ke && ws < cap; t0 += 32) {
+                            const uint64_t t = t0 + lane;
+                            const bool hit = t < ke && kp[t] == kk;
+                            const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+                            const uint64_t my = ws + __popc(hm & lanemask_lt());
+                            if (hit && my < cap) store_pair<PT>(pairs, my, uint64_t(tvals[tb + t]), pj);
+                            ws += __popc(hm);
+                        }
+                    }
+                }
+                base += round_total;
+            }
+        };
+        if (s_kst && s_pst) {
+            run(reinterpret_cast<const K*>(b_key + s_o1), reinterpret_cast<const PEnt*>(b_ent + s_o2));
+        } else {
+            run(s_kst ? reinterpret_cast<const K*>(b_key + s_o1) : tkeys + tb,
+                s_pst ? reinterpret_cast<const PEnt*>(b_ent + s_o2) : pin + q0);
+        }
+        __syncthreads();
+    }
+    // totals: matches accumulated by warp 0 lane 0; comparisons by everyone
+    compared = warp_sum(compared);
+    if (lane == 0) s_red[warp] = compared;
+    __syncthreads();
+    if (tid < 32) {
+        unsigned long long y = tid < nwarps ? s_red[tid] : 0;
+        y = warp_sum(y);
+        if (tid == 0) {
+            if (matches) atomicAdd(reinterpret_cast<unsigned long long*>(totals), matches);
+            if (y) atomicAdd(reinterpret_cast<unsigned long long*>(totals + 1), y);
+        }
+    }
+}
+
 template <typename K, typename IT>
 __global__ void k_scatter_counts(const typename EntryT<K, IT>::T* __restrict__ pin,
                                  const uint32_t* __restrict__ pcount, uint64_t m,
@@ -446,9 +732,11 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
     const size_t pscr = need_idx ? PartitionScratch<K, IT, OffT>::bytes(g, a.m)
                                  : PartitionScratch<K, void, OffT>::bytes(g, a.m);
     const size_t reorg_bytes = (a.m * ent + 255) & ~size_t(255);
-    const size_t cnt_bytes = a.pairs ? ((a.m * 4 + 255) & ~size_t(255)) : 0;
-    const size_t po_bytes = a.pairs ? (((a.m + 1) * 8 + 255) & ~size_t(255)) : 0;
-    const size_t scan_bytes = a.pairs ? ((scan_scratch_bytes(a.m) + 255) & ~size_t(255)) : 0;
+    const bool single = a.pairs && !want_counts && a.cap > 0;  // k_probe_pairs
+    const size_t cnt_bytes = (a.pairs && !single) ? ((a.m * 4 + 255) & ~size_t(255)) : 0;
+    const size_t po_bytes = single ? ((g.nparts * 8 + 255) & ~size_t(255))
+                                   : a.pairs ? (((a.m + 1) * 8 + 255) & ~size_t(255)) : 0;
+    const size_t scan_bytes = (a.pairs && !single) ? ((scan_scratch_bytes(a.m) + 255) & ~size_t(255)) : 0;
     if ((e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
                              ps_bytes + pscr + reorg_bytes + cnt_bytes + po_bytes + scan_bytes + 256,
                              s)) != cudaSuccess)
@@ -496,6 +784,27 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
                           cap, a.totals, ticket));
             return cudaGetLastError();
         };
+        // the pairs kernel reads its probe entries straight from global memory
+        // (coalesced; its second pass hits L2), so only the offsets and table
+        // keys are staged and more CTAs fit per SM
+        const size_t smem_pairs = ProbeLayout<K, OffT, E1>::bytes(P, kcap, 0);
+        auto launch_pairs = [&](auto kern, uint64_t* status) -> cudaError_t {
+            const size_t smem = smem_pairs;
+            cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 int(smem));
+            if (r != cudaSuccess) return r;
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPartProbeBlock, smem);
+            const unsigned gk = unsigned(
+                std::min<uint64_t>(uint64_t(std::max(1, per_sm)) * sms, g.nparts));
+            if ((r = cudaMemsetAsync(ticket, 0, 4, s)) != cudaSuccess) return r;
+            HG_LAUNCH("k10p_probe_pairs", s,
+                      kern<<<gk, kPartProbeBlock, smem, s>>>(
+                          static_cast<const E1*>(reorg), ppart, g.nparts, t.nv, t.seed,
+                          t.hash_kind, nv, g.pshift, offs, tkeys, tvals, kcap, 0, status,
+                          a.pairs, a.cap, a.totals, ticket));
+            return cudaGetLastError();
+        };
         if (!need_idx) {
             // count-only: key-only entries
             auto kern = k_probe_part<K, VT, OffT, void, POW2, 0, false, uint32_t>;
@@ -520,6 +829,19 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
             // per-probe counts in the caller's (original) order
             e = launch(k_probe_part<K, VT, OffT, IT, POW2, 1, true, uint32_t>, "k8p_probe_part",
                        a.counts, nullptr, nullptr, 0);
+            break;
+        }
+        if (single) {
+            // single pass: counts, look-back over partitions, pairs
+            uint64_t* status = pair_off;  // nparts status words
+            if ((e = cudaMemsetAsync(status, 0, g.nparts * sizeof(uint64_t), s)) != cudaSuccess) break;
+            if (a.pair_bytes == 4) {
+                auto kern = k_probe_pairs<K, VT, OffT, IT, POW2, uint32_t>;
+                e = launch_pairs(kern, status);
+            } else {
+                auto kern = k_probe_pairs<K, VT, OffT, IT, POW2, uint64_t>;
+                e = launch_pairs(kern, status);
+            }
             break;
         }
         // pairs: counts in partition order -> pair slots -> pairs
