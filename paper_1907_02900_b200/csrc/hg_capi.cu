@@ -55,6 +55,16 @@ bool is_device_ptr(const void* p) {
     return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
+bool is_pinned_host(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return attr.type == cudaMemoryTypeHost;
+}
+
 // A device view of a caller array: either the caller's device pointer or a
 // stream-ordered staging copy of host data (freed by release()).
 struct DevIn {
@@ -389,8 +399,14 @@ hg_status hg_probe(const hg_table* t, const void* probes, int32_t probe_width, u
     if (cudaSetDevice(t->device) != cudaSuccess) return fail(HG_ECUDA, "cudaSetDevice failed");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
 
+    // Pinned host probes without pairs: chunked pipeline, each chunk's H2D
+    // copy (on a side stream) overlaps the previous chunk's probe kernels and
+    // whatever is still running on `stream` (e.g. the build of this table).
+    constexpr uint64_t kPipeChunk = uint64_t(1) << 26;
+    const bool pipelined = m >= 2 * kPipeChunk && !opts.materialize &&
+                           probe_width == t->d.key_bytes && is_pinned_host(probes);
     DevIn pin;
-    cudaError_t e = pin.stage(probes, m * probe_width, s);
+    cudaError_t e = pipelined ? cudaSuccess : pin.stage(probes, m * probe_width, s);
     if (e != cudaSuccess) return cuda_fail(e, "hg_probe: staging probes");
     const void* dprobes = pin.ptr;
     void* widened = nullptr;
@@ -445,7 +461,49 @@ hg_status hg_probe(const hg_table* t, const void* probes, int32_t probe_width, u
     a.cap = want_pairs ? opts.pair_cap : 0;
     a.pair_offsets = pair_off;
     a.method = opts.method;
-    if (e == cudaSuccess) e = hg::probe_table(t->d, a, s);
+    if (e == cudaSuccess && !pipelined) e = hg::probe_table(t->d, a, s);
+    if (e == cudaSuccess && pipelined) {
+        void* ring = nullptr;
+        cudaStream_t cs = nullptr;
+        cudaEvent_t ready = nullptr, copied[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
+        const size_t cb = size_t(kPipeChunk) * probe_width;
+        // the ring is allocated on the copy stream, so the first copies do not
+        // wait for earlier work on `stream` (e.g. the build of this table)
+        e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaMallocAsync(&ring, 2 * cb, cs);
+        for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+            e = cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming);
+        }
+        (void)ready;
+        const char* host = static_cast<const char*>(probes);
+        for (uint64_t c = 0; e == cudaSuccess && c * kPipeChunk < m; ++c) {
+            const int b = int(c & 1);
+            const uint64_t off = c * kPipeChunk, mc = std::min(kPipeChunk, m - off);
+            char* buf = static_cast<char*>(ring) + b * cb;
+            if (c >= 2) e = cudaStreamWaitEvent(cs, done[b], 0);  // buffer free again
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(buf, host + off * probe_width, mc * probe_width,
+                                    cudaMemcpyHostToDevice, cs);
+            if (e == cudaSuccess) e = cudaEventRecord(copied[b], cs);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(s, copied[b], 0);
+            if (e != cudaSuccess) break;
+            hg::ProbeArgs ac = a;
+            ac.probes = buf;
+            ac.m = mc;
+            ac.counts = counts ? counts + off : nullptr;
+            e = hg::probe_table(t->d, ac, s);
+            if (e == cudaSuccess) e = cudaEventRecord(done[b], s);
+        }
+        if (ring) cudaFreeAsync(ring, s);
+        // destruction is deferred by the runtime until the recorded work completes
+        for (int b = 0; b < 2; ++b) {
+            if (copied[b]) cudaEventDestroy(copied[b]);
+            if (done[b]) cudaEventDestroy(done[b]);
+        }
+        if (ready) cudaEventDestroy(ready);
+        if (cs) cudaStreamDestroy(cs);
+    }
 
     hg_status st = HG_OK;
     if (e != cudaSuccess) {

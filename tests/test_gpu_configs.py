@@ -164,3 +164,26 @@ def test_c4_full_size_invariants(cuda):
     res.zero_()
     hg.probe_device(t, probes, res)
     assert int(res[0].item()) == expect
+
+
+def test_pipelined_host_probes(cuda):
+    """Pinned host probes (>= 2^27, count-only) take the chunked H2D / probe
+    pipeline of hg_probe; the results equal the device-resident probe."""
+    n, m = 1 << 24, (1 << 27) + 12345
+    keys = cuda.empty(n, dtype=cuda.int32, device="cuda")
+    hg.generate(keys, kind=0, seed=1)
+    probes = cuda.empty(m, dtype=cuda.int32, device="cuda")
+    hg.generate(probes, kind=0, seed=2)
+    # mix in hits
+    probes[: n // 2] = keys[: n // 2]
+    t = hg.build_v2(keys)
+    res = cuda.zeros(2, dtype=cuda.int64, device="cuda")
+    dcounts = cuda.zeros(m, dtype=cuda.int32, device="cuda")
+    hg.probe_device(t, probes, res, counts=dcounts)
+    hp = probes.cpu().pin_memory()
+    hcounts = np.zeros(m, np.uint32)
+    r = hg.probe_standard(t, hp, counts=hcounts)
+    assert (r.match_count, r.key_comparisons) == tuple(int(x) for x in res.cpu().tolist())
+    assert (hcounts == dcounts.cpu().numpy().view(np.uint32)).all()
+    r2 = hg.probe_standard(t, hp)
+    assert (r2.match_count, r2.key_comparisons) == (r.match_count, r.key_comparisons)
