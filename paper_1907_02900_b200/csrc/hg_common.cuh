@@ -302,4 +302,41 @@ __device__ __forceinline__ void aggregated_count(C* counter, uint32_t active, ui
     if (lane_id() == uint32_t(__ffs(peers) - 1)) red_add(counter, C(__popc(peers)));
 }
 
+// -1 when x == y and `in` (0 otherwise): one ISETP + SEL, and the caller sums
+// with IADD3 -- no dependency chain through a running count.
+template <typename K>
+__device__ __forceinline__ uint32_t eq_and(K x, K y, bool in) {
+    uint32_t d;
+    if constexpr (sizeof(K) == 4) {
+        asm("{.reg .pred p; setp.ne.u32 p, %3, 0; set.eq.and.u32.u32 %0, %1, %2, p;}"
+            : "=r"(d)
+            : "r"(x), "r"(y), "r"(uint32_t(in)));
+    } else {
+        asm("{.reg .pred p; setp.ne.u32 p, %3, 0; set.eq.and.u32.u64 %0, %1, %2, p;}"
+            : "=r"(d)
+            : "l"(x), "l"(y), "r"(uint32_t(in)));
+    }
+    return d;
+}
+
+// Matches of `key` in the segment sp[0, len) for a short segment (the caller
+// walks long ones warp-cooperatively). Segments of <= 4 entries (~99% at load
+// 1) use a fixed, predicated 4-wide compare: no loop, no divergence.
+template <typename K>
+__device__ __forceinline__ uint32_t seg_count(const K* __restrict__ sp, uint64_t len, K key) {
+    if (len <= 4) {
+        uint32_t neg = 0;
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) {
+            const bool in = q < len;
+            const K x = in ? sp[q] : K(0);
+            neg += eq_and(x, key, in);
+        }
+        return 0u - neg;
+    }
+    uint32_t c = 0;
+    for (uint32_t t = 0; t < uint32_t(len); ++t) c += sp[t] == key;
+    return c;
+}
+
 }  // namespace hg

@@ -175,23 +175,6 @@ __device__ __forceinline__ uint32_t short_pair(const K* __restrict__ pa, uint32_
     return c;
 }
 
-// -1 when x == y and `in` (0 otherwise): one ISETP + SEL, no dependency
-// chain through the running count (summed with IADD3).
-template <typename K>
-__device__ __forceinline__ uint32_t eq_and(K x, K y, bool in) {
-    uint32_t d;
-    if constexpr (sizeof(K) == 4) {
-        asm("{.reg .pred p; setp.ne.u32 p, %3, 0; set.eq.and.u32.u32 %0, %1, %2, p;}"
-            : "=r"(d)
-            : "r"(x), "r"(y), "r"(uint32_t(in)));
-    } else {
-        asm("{.reg .pred p; setp.ne.u32 p, %3, 0; set.eq.and.u32.u64 %0, %1, %2, p;}"
-            : "=r"(d)
-            : "l"(x), "l"(y), "r"(uint32_t(in)));
-    }
-    return d;
-}
-
 // Count-only segment pair with the inner side <= kShort entries (preloaded
 // under predicates) and an outer side of any (small) length.
 template <typename K>

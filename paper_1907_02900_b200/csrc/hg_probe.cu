@@ -92,8 +92,7 @@ k_probe_count(const K* __restrict__ probes, uint64_t m, uint64_t seed, int hk, D
             c[k] = 0;
             const uint64_t len = e[k] - b[k];
             compared += len;
-            if (len <= kLongSeg)
-                for (uint64_t t = b[k]; t < e[k]; ++t) c[k] += tkeys[t] == pk[k];
+            if (len <= kLongSeg) c[k] = seg_count(tkeys + b[k], len, pk[k]);
             uint32_t longm = __ballot_sync(0xffffffffu, len > kLongSeg);
             while (longm) {
                 const int src = __ffs(longm) - 1;
@@ -330,8 +329,7 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
                 const uint64_t len = e - b;
                 compared += len;
                 uint32_t c = 0;
-                if (len <= kLongSeg)
-                    for (uint64_t t = b; t < e; ++t) c += kp[t] == key;
+                if (len <= kLongSeg) c = seg_count(kp + b, len, key);
                 uint32_t longm = __ballot_sync(0xffffffffu, len > kLongSeg);
                 while (longm) {
                     const int src = __ffs(longm) - 1;
@@ -443,8 +441,7 @@ __device__ __forceinline__ uint32_t pair_count(const K* __restrict__ kp, const P
     const uint64_t len = e - b;
     compared += len;
     uint32_t c = 0;
-    if (len <= kLongSeg)
-        for (uint64_t t = b; t < e; ++t) c += kp[t] == key;
+    if (len <= kLongSeg) c = seg_count(kp + b, len, key);
     uint32_t longm = __ballot_sync(0xffffffffu, len > kLongSeg);
     while (longm) {
         const int src = __ffs(longm) - 1;
