@@ -196,8 +196,15 @@ struct SplitLayout {
     static constexpr size_t kBytes = kSplitStages * kInBytes + size_t(kTile) * (sizeof(E) + 1);
 };
 
+// CTAs per SM the layout allows (<= 227 KB of shared memory per SM): 3 when
+// the tile buffers are small, else 2; the register cap follows from it.
+template <typename K, typename VT, bool RAW>
+constexpr int split_min_blocks() {
+    return SplitLayout<K, VT, RAW>::kBytes * 3 <= size_t(220) * 1024 ? 3 : 2;
+}
+
 template <typename K, typename VT, typename OffT, bool RAW, bool PASS2, int POW2>
-__global__ void __launch_bounds__(kSplitBlock)
+__global__ void __launch_bounds__(kSplitBlock, (split_min_blocks<K, VT, RAW>()))
 k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t n, uint64_t seed,
              int hk, Divisor nv, uint32_t pshift, uint32_t dshift, uint32_t dmask, uint32_t b2,
              OffT* __restrict__ cursor, const OffT* __restrict__ part_start, uint32_t nb1,
