@@ -403,10 +403,22 @@ struct PartitionScratch {
 // out[part_start[p] .. part_start[p+1]) holds the entries of partition p
 // (p = h(key) >> pshift). part_start (nparts + 1 entries, device) receives
 // the partition offsets; part_start[nparts] = n.
+// State handed to a fused consumer when partition() stops after pass 1
+// (hg_binned.cu's k_split_build runs pass 2 and the per-partition build in
+// one kernel): the pass-1 output, the pass-2 cursors and the tile layout.
+template <typename K, typename VT, typename OffT>
+struct Pass2State {
+    const typename EntryT<K, VT>::T* mid = nullptr;
+    OffT* cur2 = nullptr;
+    const uint64_t* tile_prefix = nullptr;
+    uint32_t nb1 = 0;
+};
+
 template <typename K, typename VT, typename OffT, int POW2>
 cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, int hk,
                       const Divisor& nv, const PartGeom& g, OffT* part_start, void* scratch,
-                      typename EntryT<K, VT>::T* out, cudaStream_t s, const char* const names[3]) {
+                      typename EntryT<K, VT>::T* out, cudaStream_t s, const char* const names[3],
+                      Pass2State<K, VT, OffT>* stop_after_pass1 = nullptr) {
     using PS = PartitionScratch<K, VT, OffT>;
     using E = typename EntryT<K, VT>::T;
     char* p = static_cast<char*>(scratch);
@@ -478,6 +490,13 @@ cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, 
                   part_start, 0, nullptr, tiles1, g.nparts, mid)));
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     k_tile_prefix<OffT><<<1, 32, 0, s>>>(part_start, g.nparts, nb1, g.b2, kSplitTile, tile_prefix);
+    if (stop_after_pass1) {
+        stop_after_pass1->mid = mid;
+        stop_after_pass1->cur2 = cur2;
+        stop_after_pass1->tile_prefix = tile_prefix;
+        stop_after_pass1->nb1 = nb1;
+        return cudaGetLastError();
+    }
     const uint64_t tiles2 = tiles1 + nb1;  // upper bound; exact count = tile_prefix[nb1]
     HG_LAUNCH(names[2], s,
               (ks2<<<g2, kSplitBlock, sm2, s>>>(
