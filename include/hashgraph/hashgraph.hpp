@@ -46,6 +46,11 @@ namespace hashgraph {
 
 // ------------------------------------------------------------------ errors
 
+// keygen.hpp:75-77
+struct KeyFileError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
 namespace detail {
 
 [[noreturn]] inline void throw_status(hg_status st) {
@@ -55,6 +60,7 @@ namespace detail {
         case HG_ERANGE: throw std::out_of_range(msg);
         case HG_EOVERFLOW: throw std::overflow_error(msg);
         case HG_ENOMEM: throw std::bad_alloc();
+        case HG_EIO: throw KeyFileError(msg);
         default: throw std::runtime_error("hashgraph (B200): " + msg);
     }
 }

@@ -42,7 +42,8 @@ typedef enum hg_status {
     HG_ENOMEM = 4,
     HG_ECUDA = 5,
     HG_ENCCL = 6,
-    HG_EUNSUPPORTED = 7
+    HG_EUNSUPPORTED = 7,
+    HG_EIO = 8 /* KeyFileError (keygen.hpp:75-77): I/O or key-file format problem */
 } hg_status;
 
 typedef enum hg_hash_kind {
@@ -211,6 +212,21 @@ hg_status hg_route(const void* keys, int32_t key_width, const void* vals, int32_
  * u = (splitmix64(seed, start+i) >> 11) * 2^-53 and ref = the device CDF (n_ref doubles). */
 hg_status hg_generate(void* out, int32_t key_width, uint64_t n, int32_t kind, uint64_t seed,
                       uint64_t start, double hit, const void* ref, uint64_t n_ref, void* stream);
+
+/* Key files (keygen.hpp:97-132): 8-byte magic "HGKEYS01", little-endian u64
+ * count, then count little-endian u64 keys -- the wire format shared with the
+ * CPU reference. hg_keys_file_count validates the header and length.
+ * hg_keys_read stores the keys into `out` (host or device, key_width 8, or 4
+ * to narrow: HG_ERANGE if a key does not fit); device destinations are filled
+ * in chunks through a pinned staging buffer. cap = capacity of `out` in keys
+ * (HG_ERANGE when the file holds more). hg_keys_write writes n keys (host or
+ * device, key_width 4 or 8; u32 keys are zero-extended). Errors: HG_EIO with
+ * the reference's KeyFileError messages. */
+hg_status hg_keys_file_count(const char* path, uint64_t* count);
+hg_status hg_keys_read(const char* path, void* out, int32_t key_width, uint64_t cap, uint64_t* count,
+                       void* stream);
+hg_status hg_keys_write(const char* path, const void* keys, int32_t key_width, uint64_t n,
+                        void* stream);
 
 /* Kernel timeline (tracing): when enabled, every engine kernel launch is
  * bracketed by CUDA events on its stream. collect() waits for the recorded

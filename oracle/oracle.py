@@ -299,6 +299,10 @@ class Reference:
         lib.hgr_generate.restype = i32
         lib.hgr_generate.argtypes = [i32, u64, dbl, u64, _P]
         lib.hgr_resolve_threads.restype = C.c_uint
+        lib.hgr_write_keys.restype = i32
+        lib.hgr_write_keys.argtypes = [C.c_char_p, _P, u64]
+        lib.hgr_read_keys.restype = i32
+        lib.hgr_read_keys.argtypes = [C.c_char_p, _P, u64, _P]
         self.lib = lib
 
     @staticmethod
@@ -406,6 +410,19 @@ class Reference:
         out = np.zeros(len(counts) + 1, np.uint64)
         if self.lib.hgr_exclusive_prefix_sum(_ptr(counts), len(counts), threads, _ptr(out)):
             raise OverflowError("exclusive_prefix_sum: counter sum exceeds 64 bits")
+        return out
+
+    def write_keys(self, path, keys) -> None:
+        keys = _u64(keys)
+        if self.lib.hgr_write_keys(os.fsencode(path), _ptr(keys), len(keys)):
+            raise RuntimeError("KeyFileError")
+
+    def read_keys(self, path):
+        n = np.zeros(1, np.uint64)
+        if self.lib.hgr_read_keys(os.fsencode(path), None, 0, _ptr(n)):
+            raise RuntimeError("KeyFileError")
+        out = np.zeros(int(n[0]), np.uint64)
+        self.lib.hgr_read_keys(os.fsencode(path), _ptr(out), len(out), _ptr(n))
         return out
 
     def generate(self, kind: int, n: int, mult: float = 1.0, seed: int = 0):

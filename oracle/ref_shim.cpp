@@ -229,4 +229,26 @@ int hgr_generate(int kind, std::uint64_t n, double mult, std::uint64_t seed, std
 
 unsigned hgr_resolve_threads() { return resolve_threads(); }
 
+// write_keys / read_keys (keygen.hpp:100-130): 0 ok, 1 KeyFileError.
+int hgr_write_keys(const char* path, const std::uint64_t* keys, std::uint64_t n) {
+    try {
+        write_keys(path, std::span<const std::uint64_t>(keys, n));
+        return 0;
+    } catch (const KeyFileError&) {
+        return 1;
+    }
+}
+
+// *n = key count; keys (nullable, capacity cap) receives them.
+int hgr_read_keys(const char* path, std::uint64_t* keys, std::uint64_t cap, std::uint64_t* n) {
+    try {
+        const auto k = read_keys(path);
+        *n = k.size();
+        if (keys && k.size() <= cap) std::memcpy(keys, k.data(), k.size() * 8);
+        return 0;
+    } catch (const KeyFileError&) {
+        return 1;
+    }
+}
+
 }  // extern "C"

@@ -6,16 +6,18 @@ in include/hg_b200.h, with this package as the Python mirror of the reference
 API and the C++ mirror in include/hashgraph/.
 """
 from .hashgraph import (ENTRY_DTYPE, MATCH_PAIR_DTYPE, BuildConfig, BuildStats, ExecMode,
-                        HashGraph, IdentityHasher, InvalidArgument, JoinResult, OutOfRange,
+                        HashGraph, IdentityHasher, InvalidArgument, JoinResult, KeyFileError,
+                        OutOfRange,
                         Overflow, ProbeOptions, VertexHasher, build_v1, build_v2, count_instances,
                         derived_vertex_count, generate, hash_to_vertex, intersect_adjacency,
                         probe_device, probe_new, probe_new_device, probe_new_prepared, probe_standard,
-                        validate_csr, zipf_cdf)
+                        read_keys, validate_csr, write_keys, zipf_cdf)
 
 __all__ = [
     "ENTRY_DTYPE", "MATCH_PAIR_DTYPE", "BuildConfig", "BuildStats", "ExecMode", "HashGraph",
-    "IdentityHasher", "InvalidArgument", "JoinResult", "OutOfRange", "Overflow", "ProbeOptions",
+    "IdentityHasher", "InvalidArgument", "JoinResult", "KeyFileError", "OutOfRange", "Overflow", "ProbeOptions",
     "VertexHasher", "build_v1", "build_v2", "count_instances", "derived_vertex_count", "generate",
     "hash_to_vertex", "intersect_adjacency", "probe_device", "probe_new",
-    "probe_new_device", "probe_new_prepared", "probe_standard", "validate_csr", "zipf_cdf",
+    "probe_new_device", "probe_new_prepared", "probe_standard", "read_keys", "validate_csr", "write_keys",
+    "zipf_cdf",
 ]

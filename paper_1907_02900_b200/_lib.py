@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libhg_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "hg_b200.h")
 
-HG_OK, HG_EINVAL, HG_ERANGE, HG_EOVERFLOW, HG_ENOMEM, HG_ECUDA, HG_ENCCL, HG_EUNSUPPORTED = range(8)
+HG_OK, HG_EINVAL, HG_ERANGE, HG_EOVERFLOW, HG_ENOMEM, HG_ECUDA, HG_ENCCL, HG_EUNSUPPORTED, HG_EIO = range(9)
 HASH_MIX64, HASH_IDENTITY = 0, 1
 BUILD_SIMPLE, BUILD_BINNED = 1, 2
 
@@ -112,6 +112,9 @@ SIGNATURES = {
     "hg_shard_range": (_i32, [_u64, C.c_uint32, C.c_uint32, C.POINTER(_u64), C.POINTER(_u64)]),
     "hg_route": (_i32, [_vp, _i32, _vp, _i32, _u64, _u64, _u64, _i32, _u64, C.c_uint32, _vp, _vp,
                         _vp, _vp]),
+    "hg_keys_file_count": (_i32, [C.c_char_p, C.POINTER(_u64)]),
+    "hg_keys_read": (_i32, [C.c_char_p, _vp, _i32, _u64, C.POINTER(_u64), _vp]),
+    "hg_keys_write": (_i32, [C.c_char_p, _vp, _i32, _u64, _vp]),
     "hg_profiler_enable": (None, [_i32]),
     "hg_profiler_collect": (_i32, [C.POINTER(hg_kernel_time), _i32]),
 }

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/hg_b200.h"
 #include "hg_internal.h"
@@ -738,6 +739,167 @@ hg_status hg_generate(void* out, int32_t key_width, uint64_t n, int32_t kind, ui
     HG_CUDA(hg::generate_keys(out, key_width, n, kind, seed, start, hit, ref, n_ref,
                               static_cast<cudaStream_t>(stream)));
     return HG_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ key files
+// keygen.hpp:97-132 (HGKEYS01). Host file I/O; device destinations/sources go
+// through a pinned staging buffer in 2^24-key chunks.
+namespace {
+constexpr char kKeyMagic[8] = {'H', 'G', 'K', 'E', 'Y', 'S', '0', '1'};
+constexpr uint64_t kKeyChunk = uint64_t(1) << 24;
+
+hg_status key_header(FILE* f, const char* path, uint64_t* count) {
+    unsigned char h[16];
+    if (fseek(f, 0, SEEK_END) != 0) return fail(HG_EIO, "read failure on key file: %s", path);
+    const long sz = ftell(f);
+    if (sz < 0 || fseek(f, 0, SEEK_SET) != 0) return fail(HG_EIO, "read failure on key file: %s", path);
+    if (sz < 16 || fread(h, 1, 16, f) != 16)
+        return fail(HG_EIO, "key file too short for its header: %s", path);
+    if (std::memcmp(h, kKeyMagic, 8) != 0) return fail(HG_EIO, "key file magic mismatch: %s", path);
+    uint64_t c = 0;
+    for (int b = 0; b < 8; ++b) c |= uint64_t(h[8 + b]) << (8 * b);
+    const uint64_t payload = uint64_t(sz) - 16;
+    if (payload % 8 != 0 || payload / 8 != c)
+        return fail(HG_EIO, "key file length does not match its key count: %s", path);
+    *count = c;
+    return HG_OK;
+}
+
+struct PinnedBuf {
+    void* p = nullptr;
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+};
+}  // namespace
+
+extern "C" {
+
+hg_status hg_keys_file_count(const char* path, uint64_t* count) {
+    if (!path || !count) return fail(HG_EINVAL, "NULL argument");
+    FILE* f = fopen(path, "rb");
+    if (!f) return fail(HG_EIO, "cannot open key file: %s", path);
+    const hg_status st = key_header(f, path, count);
+    fclose(f);
+    return st;
+}
+
+hg_status hg_keys_read(const char* path, void* out, int32_t key_width, uint64_t cap, uint64_t* count,
+                       void* stream) {
+    if (!path || !count) return fail(HG_EINVAL, "NULL argument");
+    if (key_width != 4 && key_width != 8) return fail(HG_EINVAL, "key_width must be 4 or 8");
+    FILE* f = fopen(path, "rb");
+    if (!f) return fail(HG_EIO, "cannot open key file: %s", path);
+    uint64_t n = 0;
+    hg_status st = key_header(f, path, &n);
+    if (st == HG_OK && n > cap) st = fail(HG_ERANGE, "key file holds %llu keys, capacity %llu",
+                                          (unsigned long long)n, (unsigned long long)cap);
+    if (st == HG_OK && n && !out) st = fail(HG_EINVAL, "out is NULL");
+    const bool dev = st == HG_OK && n && is_device_ptr(out);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    PinnedBuf stage[2];
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    if (dev) {
+        for (int b = 0; b < 2 && st == HG_OK; ++b) {
+            if (cudaMallocHost(&stage[b].p, kKeyChunk * 8) != cudaSuccess ||
+                cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming) != cudaSuccess)
+                st = fail(HG_ENOMEM, "hg_keys_read: pinned staging");
+        }
+    }
+    std::vector<uint64_t> tmp;
+    for (uint64_t done = 0, c = 0; st == HG_OK && done < n; done += kKeyChunk, ++c) {
+        const uint64_t k = std::min(kKeyChunk, n - done);
+        const int b = int(c & 1);
+        uint64_t* buf;
+        if (dev) {
+            if (c >= 2 && cudaEventSynchronize(ev[b]) != cudaSuccess) {  // staging buffer free
+                st = fail(HG_ECUDA, "hg_keys_read: event");
+                break;
+            }
+            buf = static_cast<uint64_t*>(stage[b].p);
+        } else if (key_width == 8) {
+            buf = static_cast<uint64_t*>(out) + done;
+        } else {
+            tmp.resize(k);
+            buf = tmp.data();
+        }
+        if (fread(buf, 8, k, f) != k) {
+            st = fail(HG_EIO, "read failure on key file: %s", path);
+            break;
+        }
+        // the format is little-endian; so is every CUDA host
+        if (key_width == 4) {
+            uint32_t* o = dev ? reinterpret_cast<uint32_t*>(buf) : static_cast<uint32_t*>(out) + done;
+            for (uint64_t i = 0; i < k; ++i) {
+                if (buf[i] > 0xFFFFFFFFull) {
+                    st = fail(HG_ERANGE, "key %llu does not fit 32 bits", (unsigned long long)buf[i]);
+                    break;
+                }
+                o[i] = uint32_t(buf[i]);  // in place: o[i] never overtakes buf[i]
+            }
+            if (st != HG_OK) break;
+        }
+        if (dev) {
+            char* dst = static_cast<char*>(out) + done * key_width;
+            if (cudaMemcpyAsync(dst, buf, k * key_width, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+                cudaEventRecord(ev[b], s) != cudaSuccess) {
+                st = fail(HG_ECUDA, "hg_keys_read: copy");
+                break;
+            }
+        }
+    }
+    fclose(f);
+    if (dev) {
+        if (cudaStreamSynchronize(s) != cudaSuccess && st == HG_OK) st = fail(HG_ECUDA, "hg_keys_read: sync");
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+    if (st == HG_OK) *count = n;
+    return st;
+}
+
+hg_status hg_keys_write(const char* path, const void* keys, int32_t key_width, uint64_t n,
+                        void* stream) {
+    if (!path) return fail(HG_EINVAL, "NULL path");
+    if (key_width != 4 && key_width != 8) return fail(HG_EINVAL, "key_width must be 4 or 8");
+    if (n && !keys) return fail(HG_EINVAL, "keys is NULL");
+    FILE* f = fopen(path, "wb");
+    if (!f) return fail(HG_EIO, "cannot open key file for writing: %s", path);
+    unsigned char h[16];
+    std::memcpy(h, kKeyMagic, 8);
+    for (int b = 0; b < 8; ++b) h[8 + b] = static_cast<unsigned char>((n >> (8 * b)) & 0xff);
+    hg_status st = fwrite(h, 1, 16, f) == 16 ? HG_OK : fail(HG_EIO, "short write to key file: %s", path);
+    const bool dev = n && is_device_ptr(keys);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    PinnedBuf stage;
+    if (st == HG_OK && dev && cudaMallocHost(&stage.p, kKeyChunk * 8) != cudaSuccess)
+        st = fail(HG_ENOMEM, "hg_keys_write: pinned staging");
+    std::vector<uint64_t> wide;
+    for (uint64_t done = 0; st == HG_OK && done < n; done += kKeyChunk) {
+        const uint64_t k = std::min(kKeyChunk, n - done);
+        const char* src = static_cast<const char*>(keys) + done * key_width;
+        const void* host = src;
+        if (dev) {
+            if (cudaMemcpyAsync(stage.p, src, k * key_width, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                cudaStreamSynchronize(s) != cudaSuccess) {
+                st = fail(HG_ECUDA, "hg_keys_write: copy");
+                break;
+            }
+            host = stage.p;
+        }
+        const uint64_t* out = static_cast<const uint64_t*>(host);
+        if (key_width == 4) {
+            wide.resize(k);
+            const uint32_t* in = static_cast<const uint32_t*>(host);
+            for (uint64_t i = 0; i < k; ++i) wide[i] = in[i];
+            out = wide.data();
+        }
+        if (fwrite(out, 8, k, f) != k) st = fail(HG_EIO, "short write to key file: %s", path);
+    }
+    if (fclose(f) != 0 && st == HG_OK) st = fail(HG_EIO, "short write to key file: %s", path);
+    return st;
 }
 
 }  // extern "C"

@@ -24,6 +24,7 @@ stream.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import enum
 from dataclasses import dataclass, field
 from typing import Optional
@@ -31,7 +32,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from ._lib import (BUILD_BINNED, BUILD_SIMPLE, HASH_IDENTITY, HASH_MIX64, HG_EINVAL,
+from ._lib import (BUILD_BINNED, BUILD_SIMPLE, HASH_IDENTITY, HASH_MIX64, HG_EINVAL, HG_EIO,
                    HG_EOVERFLOW, HG_ERANGE, HashGraphError)
 
 ENTRY_DTYPE = np.dtype([("key", "<u8"), ("index", "<u8")])
@@ -40,6 +41,10 @@ MATCH_PAIR_DTYPE = np.dtype([("left_index", "<u8"), ("right_index", "<u8")])
 
 class InvalidArgument(HashGraphError, ValueError):
     """std::invalid_argument (core.hpp:106-109, join.hpp:145-147)."""
+
+
+class KeyFileError(HashGraphError, RuntimeError):
+    """keygen.hpp:75-77 (I/O or HGKEYS01 format problem)."""
 
 
 class OutOfRange(HashGraphError, IndexError):
@@ -54,7 +59,8 @@ def _check(status: int) -> None:
     if status == 0:
         return
     msg = _lib.lib().hg_last_error().decode(errors="replace")
-    cls = {HG_EINVAL: InvalidArgument, HG_ERANGE: OutOfRange, HG_EOVERFLOW: Overflow}.get(
+    cls = {HG_EINVAL: InvalidArgument, HG_ERANGE: OutOfRange, HG_EOVERFLOW: Overflow,
+           HG_EIO: KeyFileError}.get(
         status, HashGraphError)
     raise cls(status, msg)
 
@@ -556,6 +562,29 @@ def validate_csr(hg: HashGraph, expected_entries: int, input_keys=None) -> Optio
     _check(_lib.lib().hg_validate(hg.handle, ia.ptr if ia else None, int(expected_entries),
                                   C.byref(code), _stream_for(ia) if ia else None))
     return None if code.value == 0 else _VIOLATIONS.get(code.value, f"violation {code.value}")
+
+
+def write_keys(path, keys) -> None:
+    """keygen.hpp:100-111: HGKEYS01 file from host or CUDA keys (u32 keys are
+    zero-extended). Raises KeyFileError on I/O problems."""
+    ka = _Arr(keys)
+    _check(_lib.lib().hg_keys_write(os.fsencode(path), ka.ptr, ka.width, ka.n, _stream_for(ka)))
+
+
+def read_keys(path, out=None, key_width: int = 8):
+    """keygen.hpp:113-130. Returns a numpy u64 array, or fills `out` (host array
+    or CUDA tensor, key_width taken from it; device destinations are streamed
+    through pinned staging) and returns it. Raises KeyFileError on any I/O or
+    format problem, OutOfRange when `out` is too small or a key does not fit."""
+    p = os.fsencode(path)
+    if out is None:
+        n = C.c_uint64(0)
+        _check(_lib.lib().hg_keys_file_count(p, C.byref(n)))
+        out = np.zeros(n.value, np.uint64 if key_width == 8 else np.uint32)
+    oa = _Arr(out)
+    got = C.c_uint64(0)
+    _check(_lib.lib().hg_keys_read(p, oa.ptr, oa.width, oa.n, C.byref(got), _stream_for(oa)))
+    return out[: got.value] if got.value != oa.n else out
 
 
 def zipf_cdf(ranks: int, s: float) -> np.ndarray:

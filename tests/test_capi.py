@@ -4,6 +4,7 @@ derivation, errors) follow the reference. No compute calls without a GPU."""
 import ctypes as C
 import subprocess
 
+import numpy as np
 import pytest
 
 from paper_1907_02900_b200 import _lib
@@ -73,3 +74,39 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(_lib.HashGraphError) as ei:
         hg.build_v1([1, 2, 3])
     assert ei.value.status == _lib.HG_ECUDA
+
+
+def test_key_files_match_the_reference(tmp_path, reference):
+    """HGKEYS01 (keygen.hpp:97-132): files written by the engine are read by the
+    reference and vice versa; format errors raise KeyFileError (host paths only,
+    no GPU needed)."""
+    import paper_1907_02900_b200 as hg
+    rng = np.random.default_rng(5)
+    keys = rng.integers(0, 1 << 63, size=100003, dtype=np.uint64)
+    keys[:3] = [0, 0xFFFFFFFFFFFFFFFF, 7]
+    a = str(tmp_path / "a.keys")
+    hg.write_keys(a, keys)
+    assert (reference.read_keys(a) == keys).all()
+    b = str(tmp_path / "b.keys")
+    reference.write_keys(b, keys[:777])
+    assert open(a, "rb").read()[:8] == b"HGKEYS01"
+    assert (hg.read_keys(b) == keys[:777]).all()
+    # u32 in and out (zero-extended on write, range-checked on read)
+    small = keys[:50] & np.uint64(0xFFFFFFFF)
+    hg.write_keys(b, small.astype(np.uint32))
+    assert (reference.read_keys(b) == small).all()
+    assert (hg.read_keys(b, key_width=4) == small.astype(np.uint32)).all()
+    with pytest.raises(hg.OutOfRange):
+        hg.read_keys(a, key_width=4)
+    # empty file round trip
+    hg.write_keys(b, np.zeros(0, np.uint64))
+    assert len(hg.read_keys(b)) == 0 and len(reference.read_keys(b)) == 0
+    # format errors (keygen.hpp:117-126)
+    bad = tmp_path / "bad.keys"
+    for blob in (b"HGKEYS0", b"XXKEYS01" + bytes(8), b"HGKEYS01" + (2).to_bytes(8, "little") + bytes(8),
+                 b"HGKEYS01" + (1).to_bytes(8, "little") + bytes(9)):
+        bad.write_bytes(blob)
+        with pytest.raises(hg.KeyFileError):
+            hg.read_keys(str(bad))
+    with pytest.raises(hg.KeyFileError):
+        hg.read_keys(str(tmp_path / "missing.keys"))

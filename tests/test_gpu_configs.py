@@ -205,3 +205,23 @@ def test_fused_split_build_opt_in(oracle, cuda, monkeypatch):
     host = keys.cpu().numpy().view(np.uint32).astype(np.uint64)
     t = hg.build_v2(keys)
     canon_equal(t, oracle.build(host, variant=2))
+
+
+def test_key_files_device(tmp_path, cuda):
+    """HGKEYS01 straight to / from device memory (pinned staging chunks), then
+    a build from the loaded keys equals the build from the originals."""
+    n = (1 << 25) + 3
+    keys = cuda.empty(n, dtype=cuda.int64, device="cuda")
+    hg.generate(keys, kind=0, seed=4)
+    path = str(tmp_path / "k.keys")
+    hg.write_keys(path, keys)
+    back = cuda.zeros(n, dtype=cuda.int64, device="cuda")
+    hg.read_keys(path, out=back)
+    assert bool((back == keys).all())
+    small = cuda.zeros(n, dtype=cuda.int32, device="cuda")
+    keys32 = (keys & 0x7FFFFFFF).to(cuda.int32)
+    hg.write_keys(path, keys32)
+    hg.read_keys(path, out=small)
+    assert bool((small == keys32).all())
+    t1, t2 = hg.build_v2(keys32), hg.build_v2(small)
+    assert (t1.offsets() == t2.offsets()).all()
