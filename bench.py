@@ -485,6 +485,38 @@ def run_b200(args):
                        "path": "hashgraph.build_v2/probe_standard -> C-ABI hg_build/hg_probe "
                                "with pinned host buffers"}
 
+    # ---- e2e at N > 1: every rank stages its pinned host slice (H2D inside
+    # the timed region), runs the sharded step through ShardedHashGraph and
+    # reads the global totals back; max over ranks
+    if not args.no_e2e and world > 1:
+        hkeys = keys.cpu().pin_memory()
+        hprobes = probes.cpu().pin_memory()
+        dk, dp = torch.empty_like(keys), torch.empty_like(probes)
+
+        def e2e_step():
+            dk.copy_(hkeys, non_blocking=True)
+            dp.copy_(hprobes, non_blocking=True)
+            engine.build_and_probe(dk, dp, result)
+            return result.cpu()
+
+        e2e_step()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            r = e2e_step()
+        f1.record(stream)
+        barrier()
+        e_ms = torch.tensor([f0.elapsed_time(f1) / args.steps], device=dev)
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e_ms = float(e_ms.item())
+        assert int(r[0]) == matches, "e2e result differs from device-resident result"
+        line["e2e"] = {"value": round(world * (n + m) / (e_ms * 1e-3) / 1e9, 3), "unit": "Gkeys/s",
+                       "ms_per_step": round(e_ms, 3), "h2d_bytes_per_step": 4 * (n + m) * world,
+                       "d2h_bytes_per_step": 16 * world,
+                       "path": "pinned host slices -> ShardedHashGraph.build_and_probe (C-ABI "
+                               "hg_route / hg_build / hg_probe, NCCL all_to_all) -> totals"}
+
     if not args.no_cpu and world == 1 and rank == 0:
         try:
             cb = cpu_reference_rate(args.variant, args.cpu_log2n, trials=5, warmup=1)
