@@ -111,7 +111,11 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
         const bool staged = cntp <= cap;
         const uint64_t vb = p << pshift;
         const uint32_t pv = uint32_t(nv_total - vb < P ? nv_total - vb : uint64_t(P));
-        for (uint32_t j = tid; j < pv; j += kBuildBlock) cnt[j] = 0;
+        if ((pv & 3) == 0) {
+            for (uint32_t j = 4 * tid; j < pv; j += 4 * kBuildBlock) sts128(cnt + j, make_uint4(0, 0, 0, 0));
+        } else {
+            for (uint32_t j = tid; j < pv; j += kBuildBlock) cnt[j] = 0;
+        }
         E ent[kItems];
         if (staged) {
             mbar_wait(&s_bar, phase);
@@ -162,6 +166,9 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
         const uint32_t per = (pv + kBuildBlock - 1) / kBuildBlock;
         const uint32_t j0 = min(pv, tid * per), j1 = min(pv, j0 + per);
         const bool vec = (per & 3) == 0 && j1 - j0 == per && per <= 16;
+        // u32 offsets of a partition whose width is a multiple of 4 are written
+        // after the scan as lane-contiguous 16-byte stores (block-uniform)
+        const bool coal = sizeof(OffT) == 4 && (pv & 3) == 0;
         uint32_t run = 0;
         if (vec) {
             for (uint32_t q = 0; q < per; q += 4) {
@@ -198,12 +205,7 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
                                             acc + c4.x + c4.y + c4.z);
                 sts128(cnt + j0 + q, st);
                 const uint32_t nxt = st.w + c4.w;
-                if constexpr (sizeof(OffT) == 4) {
-                    // offs + 1 is 16-byte aligned (hg_capi pads it); vb + j0 + q is a multiple of 4
-                    *reinterpret_cast<uint4*>(offs + vb + j0 + q + 1) =
-                        make_uint4(uint32_t(s) + st.y, uint32_t(s) + st.z, uint32_t(s) + st.w,
-                                   uint32_t(s) + nxt);
-                } else {
+                if (!coal) {
                     offs[vb + j0 + q + 1] = OffT(s + st.y);
                     offs[vb + j0 + q + 2] = OffT(s + st.z);
                     offs[vb + j0 + q + 3] = OffT(s + st.w);
@@ -216,13 +218,24 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
                 const uint32_t c = cnt[j];
                 cnt[j] = acc;  // exclusive start
                 acc += c;
-                offs[vb + j + 1] = OffT(s + acc);  // end(j)
+                if (!coal) offs[vb + j + 1] = OffT(s + acc);  // end(j)
             }
         }
         if (p == 0 && tid == 0) offs[0] = 0;
         // the previous partition's bulk stores must have read the staging arrays
         if (tid == 0) bulk_wait_read();
         __syncthreads();
+        if (coal) {
+            // end(j) = start(j+1) from the exclusive starts now in cnt (offs + 1
+            // is 16-byte aligned, hg_capi pads it; vb + 4c is a multiple of 4)
+            for (uint32_t c = tid; 4 * c < pv; c += kBuildBlock) {
+                const uint4 st = lds128(cnt + 4 * c);
+                const uint32_t nxt = 4 * c + 4 < pv ? cnt[4 * c + 4] : cntp;
+                *reinterpret_cast<uint4*>(offs + vb + 4 * c + 1) =
+                    make_uint4(uint32_t(s) + st.y, uint32_t(s) + st.z, uint32_t(s) + st.w,
+                               uint32_t(s) + nxt);
+            }
+        }
         if (staged) {
             K* skp = sk + (s & (KA - 1));
             VT* svp = sv + (s & (VA - 1));

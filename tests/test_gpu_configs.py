@@ -225,3 +225,15 @@ def test_key_files_device(tmp_path, cuda):
     assert bool((small == keys32).all())
     t1, t2 = hg.build_v2(keys32), hg.build_v2(small)
     assert (t1.offsets() == t2.offsets()).all()
+
+
+@pytest.mark.parametrize("tail", [4000, 2052, 100, 4092, 1540, 1541, 4096])
+def test_partial_last_partition(oracle, cuda, tail):
+    """V = 1023 * 4096 + tail: the last K7 partition is partial (vectorised
+    scan for some threads, scalar for others; coalesced u32 offset stores)."""
+    nv = 1023 * 4096 + tail
+    rng = np.random.default_rng(tail)
+    keys = rng.integers(0, 1 << 32, size=nv, dtype=np.uint64)
+    t = hg.build_v2(keys.astype(np.uint32), vertex_count=nv)
+    o = oracle.build(keys, variant=2, vertex_count=nv)
+    canon_equal(t, o)
