@@ -138,20 +138,30 @@ k_part_hist(const K* __restrict__ keys, uint64_t n, uint64_t seed, int hk, Divis
     if (gtid < head) count(keys[gtid]);
     const uint64_t nvec = (n - head) / VEC;
     const V* body = reinterpret_cast<const V*>(keys + head);
+    // two 16-byte vectors per step, software-pipelined one step ahead so the
+    // loads of step i+1 are in flight while step i's keys are counted
     uint64_t q = gtid;
+    V a{}, b{};
+    if (q + stride < nvec) {
+        a = __ldcs(body + q);
+        b = __ldcs(body + q + stride);
+    }
     for (; q + stride < nvec; q += 2 * stride) {
-        const V a = __ldcs(body + q);
-        const V b = __ldcs(body + q + stride);
-        const K* ka = reinterpret_cast<const K*>(&a);
-        const K* kb = reinterpret_cast<const K*>(&b);
+        const V ca = a, cb = b;
+        if (q + 3 * stride < nvec) {
+            a = __ldcs(body + q + 2 * stride);
+            b = __ldcs(body + q + 3 * stride);
+        }
+        const K* ka = reinterpret_cast<const K*>(&ca);
+        const K* kb = reinterpret_cast<const K*>(&cb);
 #pragma unroll
         for (int k = 0; k < VEC; ++k) count(ka[k]);
 #pragma unroll
         for (int k = 0; k < VEC; ++k) count(kb[k]);
     }
     if (q < nvec) {
-        const V a = __ldcs(body + q);
-        const K* ka = reinterpret_cast<const K*>(&a);
+        const V a1 = __ldcs(body + q);
+        const K* ka = reinterpret_cast<const K*>(&a1);
 #pragma unroll
         for (int k = 0; k < VEC; ++k) count(ka[k]);
     }
