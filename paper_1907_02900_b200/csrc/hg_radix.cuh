@@ -181,7 +181,7 @@ constexpr int kSplitStages = 2;  // TMA input stages (one tile prefetched ahead)
 constexpr int kMaxDigits = 256;
 // 4096-entry tiles for <= 8-byte entries, 2048 for 16-byte ones.
 template <typename E>
-__host__ __device__ constexpr int split_items() { return sizeof(E) >= 16 ? 4 : 8; }
+__host__ __device__ constexpr int split_items() { return sizeof(E) >= 16 ? 4 : sizeof(E) <= 4 ? 16 : 8; }
 template <typename E>
 __host__ __device__ constexpr int split_tile() { return kSplitBlock * split_items<E>(); }
 
