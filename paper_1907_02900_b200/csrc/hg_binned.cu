@@ -430,7 +430,6 @@ k_split_build(const typename EntryT<K, VT>::T* __restrict__ mid, OffT* __restric
         s_defer = 0;
     }
     uint32_t ph[2] = {0, 0};
-    uint64_t discards = 0;
     for (uint32_t it = 0;; ++it) {
         const int st = int(it & 1);
         __syncthreads();  // s_task[st] published; previous task fully done
@@ -644,7 +643,6 @@ k_split_build(const typename EntryT<K, VT>::T* __restrict__ mid, OffT* __restric
         }
     }
     if (tid == 0) bulk_wait_all();
-    (void)discards;
 }
 
 // ---------------------------------------------------------------- K7b

@@ -28,7 +28,6 @@
 //                     subset; ours is the sequential one).
 // key_comparisons = sum_v |A_v|*|B_v| (join.hpp:52, test_join.cpp:189-205).
 #include <algorithm>
-#include <cstdlib>
 
 #include "hg_common.cuh"
 #include "hg_internal.h"
@@ -61,7 +60,6 @@ struct IsArgs {
     uint64_t cap;
     uint64_t* totals;  // [0] match_count, [1] key_comparisons
     uint32_t* ticket;
-    int dbg;           // experiment knob (HG_IS_DBG): 1 = skip the compare phase
 };
 
 __device__ __forceinline__ uint64_t ld_val(const void* p, int val8, uint64_t i) {
@@ -279,7 +277,6 @@ __device__ __forceinline__ void intersect_tile(const IsArgs& a, const OA* soa, c
     // (in place) the vertices that matched, for the write pass.
     compared += cmp_tile;
     uint32_t nq2 = 0;
-    if (a.dbg == 1) nq = 0;
     for (uint32_t k0 = 0; k0 < nq; k0 += 32) {
         const uint32_t k = k0 + lane;
         const bool act = k < nq;
@@ -552,7 +549,6 @@ static cudaError_t intersect_impl(const TableDesc& A, const TableDesc& B, const 
     a.pair8 = ia.pair_bytes == 8;
     a.cap = ia.pairs ? ia.cap : 0;
     a.totals = ia.totals;
-    a.dbg = getenv("HG_IS_DBG") ? atoi(getenv("HG_IS_DBG")) : 0;
     // staged key capacity per side: ~1.25x the mean slice + slack (a uniform
     // tile exceeds it with negligible probability), within a 12 KB per side
     // and stage budget; larger slices are read from global memory

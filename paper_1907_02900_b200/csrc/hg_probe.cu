@@ -457,6 +457,21 @@ __device__ __forceinline__ uint32_t pair_count(const K* __restrict__ kp, const P
     return c;
 }
 
+constexpr uint32_t kNeedWalk = 0xFFFFFFFFu;
+
+// Pass-A summary of one probe for pass B: 0 (no match), (t << 16) | 1 (one
+// match at tile key t, short segment, t < 2^16) or kNeedWalk.
+template <typename K>
+__device__ __forceinline__ uint32_t pair_info(const K* __restrict__ kp, K key, uint64_t b, uint64_t e,
+                                              uint32_t c) {
+    if (c == 0) return 0u;
+    if (c != 1 || e - b > kLongSeg || e > 0xFFFFu) return kNeedWalk;
+    uint32_t th = uint32_t(b);
+    for (uint64_t t = b; t < e; ++t)
+        if (kp[t] == key) th = uint32_t(t);
+    return (th << 16) | 1u;
+}
+
 template <typename K, typename VT, typename OffT, typename IT, int POW2, typename PT>
 __global__ void __launch_bounds__(kPartProbeBlock)
 k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __restrict__ ppart,
@@ -474,6 +489,9 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
     unsigned char* const b_off = smem;
     unsigned char* const b_key = smem + L::off_bytes(P);
     unsigned char* const b_ent = b_key + L::key_bytes(kcap);
+    // per-probe result of pass A for the current round: 0 = no match,
+    // (t << 16) | 1 = exactly one match at tile key t, kNeedWalk = walk again
+    uint32_t* const s_info = reinterpret_cast<uint32_t*>(b_ent + L::ent_bytes(pcap));
     __shared__ uint64_t s_bar;
     __shared__ uint64_t s_p, s_tb, s_q0, s_q1, s_base;
     __shared__ uint32_t s_o0, s_o1, s_o2, s_kst, s_pst;
@@ -546,7 +564,10 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
                 const uint32_t c = pair_count<K, OffT, PEnt, PE, POW2>(kp, cur, soff, i, qn, tb, vb, seed,
                                                                         hk, nv, compared, key, b, e);
                 const uint32_t cw = warp_sum(c);
-                if (ch < kPairRound && lane == 0) s_wt[ch * nwarps + warp] = cw;
+                if (ch < kPairRound) {
+                    if (lane == 0) s_wt[ch * nwarps + warp] = cw;
+                    s_info[ch * kPartProbeBlock + i0] = pair_info(kp, key, b, e, c);
+                }
                 mine += cw;
             }
             if (lane == 0) s_red[warp] = mine;
@@ -597,6 +618,7 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
                             kp, cur, soff, i, qn, tb, vb, seed, hk, nv, dummy, key, b, e);
                         const uint32_t cw = warp_sum(c);
                         if (lane == 0) s_wt[(ch - r0) * nwarps + warp] = cw;
+                        s_info[(ch - r0) * kPartProbeBlock + warp * 32 + lane] = pair_info(kp, key, b, e, c);
                     }
                 }
                 __syncthreads();
@@ -626,20 +648,25 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
                     const uint64_t i = ch * kPartProbeBlock + warp * 32 + lane;
                     const PEnt cur = nxtb;
                     if (ch + 1 < r1 && i + kPartProbeBlock < qn) nxtb = ep[i + kPartProbeBlock];
-                    const uint32_t c = pair_count<K, OffT, PEnt, PE, POW2>(
-                        kp, cur, soff, i, qn, tb, vb, seed, hk, nv, dummy, key, b, e);
+                    const uint32_t info = i < qn ? s_info[(ch - r0) * kPartProbeBlock + warp * 32 + lane] : 0u;
+                    const bool walk = info == kNeedWalk;
+                    uint32_t c = info & 1u;
+                    b = e = 0;
+                    key = 0;
+                    if (__any_sync(0xffffffffu, walk)) {
+                        // duplicates / long segments: count again (warp-collective)
+                        const uint32_t cc = pair_count<K, OffT, PEnt, PE, POW2>(
+                            kp, cur, soff, i, qn, tb, vb, seed, hk, nv, dummy, key, b, e);
+                        if (walk) c = cc;
+                    }
+                    if (!walk) b = e = 0;
                     const uint32_t incl = warp_inclusive_sum(c);
                     uint64_t sl = base + s_wt[(ch - r0) * nwarps + warp] + (incl - c);
                     const uint64_t len = e - b;
                     const uint64_t pidx = PE::kHasVal && i < qn ? uint64_t(PE::val(cur)) : 0;
-                    if (c == 1 && len <= kLongSeg) {
-                        // common case (unique build keys): locate the hit in shared
-                        // memory first, so the value gather and the store are one
-                        // round trip for the whole warp instead of one per step
-                        uint64_t th = b;
-                        for (uint64_t t = b; t < e; ++t)
-                            if (kp[t] == key) th = t;
-                        if (sl < cap) store_pair<PT>(pairs, sl, uint64_t(tvals[tb + th]), pidx);
+                    if (!walk && c == 1) {
+                        // one match at a known tile key: one value gather + store
+                        if (sl < cap) store_pair<PT>(pairs, sl, uint64_t(tvals[tb + (info >> 16)]), pidx);
                     } else if (c && len <= kLongSeg) {
                         for (uint64_t t = b; t < e && sl < cap; ++t) {
                             if (kp[t] == key) {
@@ -784,7 +811,8 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
         // the pairs kernel reads its probe entries straight from global memory
         // (coalesced; its second pass hits L2), so only the offsets and table
         // keys are staged and more CTAs fit per SM
-        const size_t smem_pairs = ProbeLayout<K, OffT, E1>::bytes(P, kcap, 0);
+        const size_t smem_pairs = ProbeLayout<K, OffT, E1>::bytes(P, kcap, 0) +
+                                  size_t(kPairRound) * kPartProbeBlock * sizeof(uint32_t);
         auto launch_pairs = [&](auto kern, uint64_t* status) -> cudaError_t {
             const size_t smem = smem_pairs;
             cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
