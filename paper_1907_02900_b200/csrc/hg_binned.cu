@@ -656,18 +656,7 @@ k_split_build(const typename EntryT<K, VT>::T* __restrict__ mid, OffT* __restric
 //               prefix (the placement cursor)
 //   k7b_place   grid-stride again; aggregated tickets on the cursors leave
 //               offs[v+1] = end(v) and give each entry its slot
-template <typename OffT>
-__global__ void k7b_prefix(const OffT* __restrict__ part_start, const uint32_t* __restrict__ list,
-                           const uint32_t* __restrict__ big_n, uint64_t* __restrict__ pref) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const uint32_t nb = *big_n;
-    uint64_t acc = 0;
-    for (uint32_t i = 0; i < nb; ++i) {
-        pref[i] = acc;
-        acc += uint64_t(part_start[list[i] + 1]) - uint64_t(part_start[list[i]]);
-    }
-    pref[nb] = acc;
-}
+constexpr uint32_t kBigChunk = 4096;  // entries of a queued partition per K7b CTA task
 
 // Queued entry g -> (partition index in the list, entry position).
 __device__ __forceinline__ uint32_t big_owner(const uint64_t* pref, uint32_t nb, uint64_t g) {
@@ -678,6 +667,92 @@ __device__ __forceinline__ uint32_t big_owner(const uint64_t* pref, uint32_t nb,
     }
     return lo;
 }
+
+template <typename OffT>
+__global__ void k7b_prefix(const OffT* __restrict__ part_start, const uint32_t* __restrict__ list,
+                           const uint32_t* __restrict__ big_n, uint64_t* __restrict__ pref,
+                           uint64_t* __restrict__ cpref) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const uint32_t nb = *big_n;
+    uint64_t acc = 0, cacc = 0;
+    for (uint32_t i = 0; i < nb; ++i) {
+        pref[i] = acc;
+        cpref[i] = cacc;
+        const uint64_t sz = uint64_t(part_start[list[i] + 1]) - uint64_t(part_start[list[i]]);
+        acc += sz;
+        cacc += (sz + kBigChunk - 1) / kBigChunk;
+    }
+    pref[nb] = acc;
+    cpref[nb] = cacc;
+}
+
+// Block-aggregated variant for partitions of <= 2^14 vertices: a CTA takes a
+// 4096-entry chunk of one queued partition, counts it per vertex in shared
+// memory (warp-aggregated shared atomics), and touches the global counters /
+// cursors once per (chunk, vertex) instead of once per entry or warp -- a
+// hot key costs one global atomic per chunk. PLACE: the chunk reserves each
+// vertex's run with one global atomic, then hands out slots from shared
+// memory.
+template <typename K, typename VT, typename OffT, int POW2, bool PLACE>
+__global__ void __launch_bounds__(512)
+k7b_chunk(const typename EntryT<K, VT>::T* __restrict__ reorg, const OffT* __restrict__ part_start,
+          const uint32_t* __restrict__ list, const uint32_t* __restrict__ big_n,
+          const uint64_t* __restrict__ cpref, uint64_t nv_total, uint64_t seed, Divisor nv,
+          uint32_t pshift, OffT* __restrict__ offs, K* __restrict__ okeys, VT* __restrict__ ovals) {
+    using PE = EntryT<K, VT>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    OffT* const hist = reinterpret_cast<OffT*>(smem);
+    const uint32_t nb = *big_n;
+    if (nb == 0) return;
+    const uint64_t nchunks = cpref[nb];
+    const uint32_t tid = threadIdx.x;
+    const uint64_t P = uint64_t(1) << pshift;
+    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        const uint32_t li = big_owner(cpref, nb, c);
+        const uint64_t p = list[li];
+        const uint64_t s = part_start[p], e = part_start[p + 1];
+        const uint64_t c0 = s + (c - cpref[li]) * kBigChunk;
+        const uint64_t c1 = e < c0 + kBigChunk ? e : c0 + kBigChunk;
+        const uint64_t vb = p << pshift;
+        const uint32_t pv = uint32_t(nv_total - vb < P ? nv_total - vb : P);
+        for (uint32_t v = tid; v < pv; v += blockDim.x) hist[v] = 0;
+        __syncthreads();
+        for (uint64_t j0 = c0; j0 < c1; j0 += blockDim.x) {
+            const uint64_t j = j0 + tid;
+            const bool act = j < c1;
+            const uint32_t active = __ballot_sync(0xffffffffu, act);
+            if (act) {
+                const uint32_t lv = uint32_t(vhash<POW2>(PE::key(reorg[j]), seed, nv) - vb);
+                aggregated_count<true>(hist + lv, active, lv);
+            }
+        }
+        __syncthreads();
+        for (uint32_t v = tid; v < pv; v += blockDim.x) {
+            const OffT h = hist[v];
+            if (h) {
+                const OffT base = atom_add(offs + vb + v + 1, h);
+                if constexpr (PLACE) hist[v] = base;
+            }
+        }
+        if constexpr (PLACE) {
+            __syncthreads();
+            for (uint64_t j0 = c0; j0 < c1; j0 += blockDim.x) {
+                const uint64_t j = j0 + tid;
+                const bool act = j < c1;
+                const uint32_t active = __ballot_sync(0xffffffffu, act);
+                if (act) {
+                    const auto en = reorg[j];
+                    const uint32_t lv = uint32_t(vhash<POW2>(PE::key(en), seed, nv) - vb);
+                    const uint64_t slot = aggregated_ticket<true>(hist + lv, active, lv);
+                    okeys[slot] = PE::key(en);
+                    ovals[slot] = PE::val(en);
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
 
 template <typename K, typename VT, typename OffT, int POW2, bool PLACE>
 __global__ void __launch_bounds__(256)
@@ -783,7 +858,7 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
     const size_t reorg_bytes = (t.n * sizeof(E) + 255) & ~size_t(255);
     // K7b queue: at most nparts oversized partitions
     const size_t list_bytes = ((g.nparts + 1) * 4 + 255) & ~size_t(255);
-    const size_t pref_bytes = ((g.nparts + 1) * 8 + 255) & ~size_t(255);
+    const size_t pref_bytes = (2 * (g.nparts + 1) * 8 + 255) & ~size_t(255);  // pref | cpref
     char* scratch = nullptr;
     if ((e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
                              ps_bytes + pscr + reorg_bytes + list_bytes + pref_bytes + 2048, s)) !=
@@ -851,8 +926,36 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
         // oversized partitions (device-side count; the kernels exit at once
         // when there are none)
         uint32_t* big_n = ticket + 1;
-        k7b_prefix<OffT><<<1, 32, 0, s>>>(part_start, big_list, big_n, big_pref);
+        uint64_t* big_cpref = big_pref + g.nparts + 1;
+        k7b_prefix<OffT><<<1, 32, 0, s>>>(part_start, big_list, big_n, big_pref, big_cpref);
         const unsigned gb = unsigned(num_sms() * 8);
+        // block-aggregated K7b when a partition's counters fit shared memory
+        const size_t hsm = (size_t(1) << g.pshift) * sizeof(OffT);
+        const bool chunked = hsm <= (size_t(64) << 10);
+        if (chunked) {
+            auto kc0 = k7b_chunk<K, VT, OffT, POW2, false>;
+            auto kc1 = k7b_chunk<K, VT, OffT, POW2, true>;
+            if (hsm > (size_t(48) << 10) &&
+                ((e = cudaFuncSetAttribute(kc0, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hsm))) !=
+                     cudaSuccess ||
+                 (e = cudaFuncSetAttribute(kc1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hsm))) !=
+                     cudaSuccess))
+                break;
+            const unsigned gc = unsigned(num_sms() * 3);
+            HG_LAUNCH("k7b_big_count", s,
+                      (kc0<<<gc, 512, hsm, s>>>(reorg, part_start, big_list, big_n, big_cpref, t.nv,
+                                               t.seed, nv, g.pshift, offs, nullptr, nullptr)));
+            HG_LAUNCH("k7b_big_scan", s,
+                      (k7b_scan<OffT><<<unsigned(num_sms() * 2), 1024, 0, s>>>(part_start, big_list,
+                                                                           big_n, t.nv, g.pshift,
+                                                                           offs)));
+            HG_LAUNCH("k7b_big_place", s,
+                      (kc1<<<gc, 512, hsm, s>>>(reorg, part_start, big_list, big_n, big_cpref, t.nv,
+                                               t.seed, nv, g.pshift, offs, static_cast<K*>(t.keys),
+                                               static_cast<VT*>(t.vals))));
+            e = cudaGetLastError();
+            break;
+        }
         HG_LAUNCH("k7b_big_count", s,
                   (k7b_pass<K, VT, OffT, POW2, false><<<gb, 256, 0, s>>>(
                       reorg, part_start, big_list, big_n, big_pref, t.seed, nv, g.pshift, offs,
