@@ -237,3 +237,38 @@ def test_partial_last_partition(oracle, cuda, tail):
     t = hg.build_v2(keys.astype(np.uint32), vertex_count=nv)
     o = oracle.build(keys, variant=2, vertex_count=nv)
     canon_equal(t, o)
+
+
+def test_sharded_engine_over_nccl_world1(cuda, oracle):
+    """The N > 1 bench path end to end on one GPU: ShardedHashGraph over a
+    world-1 NCCL group (hg_route, count all_gather, all_to_all_single, shard
+    build with vertex_base, routed probe, all_reduce) equals the unsharded
+    build and probe; export_global rebases offsets like the reference."""
+    import socket
+    import torch.distributed as dist
+    from paper_1907_02900_b200 import sharded
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=cuda.device("cuda", 0))
+    try:
+        n = 1 << 22
+        keys = cuda.empty(n, dtype=cuda.int32, device="cuda")
+        probes = cuda.empty(n, dtype=cuda.int32, device="cuda")
+        hg.generate(keys, kind=0, seed=1)
+        hg.generate(probes, kind=0, seed=2)
+        eng = sharded.ShardedHashGraph(1, 0, variant=2)
+        st = eng.build(keys, 0, n)
+        off, k, v = eng.export_global()
+        o = oracle.build(keys.cpu().numpy().view(np.uint32).astype(np.uint64), variant=2)
+        assert (off == o.offsets).all()
+        tot = eng.probe_count(probes, 0)
+        ref = hg.probe_standard(hg.build_v2(keys), probes)
+        assert tuple(int(x) for x in tot.cpu().tolist()) == (ref.match_count, ref.key_comparisons)
+        res = cuda.zeros(2, dtype=cuda.int64, device="cuda")
+        eng.build_and_probe(keys, probes, res)
+        assert int(res[0]) == ref.match_count
+        del st
+    finally:
+        dist.destroy_process_group()
