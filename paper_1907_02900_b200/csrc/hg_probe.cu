@@ -312,69 +312,104 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
         // shared memory: LDS on 32-bit addresses) and for oversized slices
         // (generic loads from global memory).
         auto run = [&](const K* __restrict__ kp, const PEnt* __restrict__ ep) {
-            for (uint64_t base = uint64_t(warp) * 32; base < qn; base += uint64_t(nwarps) * 32) {
-                const uint64_t i = base + lane;
-                const bool valid = i < qn;
-                K key = 0;
-                typename std::conditional<std::is_void<IT>::value, uint32_t, IT>::type pidx = 0;
-                uint64_t b = 0, e = 0;
-                if (valid) {
-                    const auto ent = ep[i];
-                    key = PE::key(ent);
-                    if constexpr (PE::kHasVal) pidx = PE::val(ent);
-                    const uint32_t lv = uint32_t(hv<POW2>(key, seed, hk, nv) - vb);
-                    b = uint64_t(soff[lv]) - tb;
-                    e = uint64_t(soff[lv + 1]) - tb;
+            if constexpr (MODE == 0) {
+                // count-only (the C2 step): partition-relative indices in the
+                // offsets' width (u32 at C2), fewer 64-bit address updates
+                using I = OffT;
+                const I qi = I(qn), tbi = I(tb);
+                for (I base = I(warp) * 32; base < qi; base += I(nwarps) * 32) {
+                    const I i = base + I(lane);
+                    K key = 0;
+                    I b = 0, e = 0;
+                    if (i < qi) {
+                        key = PE::key(ep[i]);
+                        const uint32_t lv = uint32_t(hv<POW2>(key, seed, hk, nv) - vb);
+                        b = I(soff[lv]) - tbi;
+                        e = I(soff[lv + 1]) - tbi;
+                    }
+                    const I len = e - b;
+                    compared += len;
+                    uint32_t c = 0;
+                    if (len <= I(kLongSeg)) c = seg_count(kp + b, uint64_t(len), key);
+                    uint32_t longm = __ballot_sync(0xffffffffu, len > I(kLongSeg));
+                    while (longm) {
+                        const int src = __ffs(longm) - 1;
+                        longm &= longm - 1;
+                        const I kb = __shfl_sync(0xffffffffu, b, src);
+                        const I ke = __shfl_sync(0xffffffffu, e, src);
+                        const K kk = __shfl_sync(0xffffffffu, key, src);
+                        uint32_t cc = 0;
+                        for (I t = kb + I(lane); t < ke; t += 32) cc += kp[t] == kk;
+                        cc = warp_sum(cc);
+                        if (int(lane) == src) c = cc;
+                    }
+                    matches += c;
                 }
-                const uint64_t len = e - b;
-                compared += len;
-                uint32_t c = 0;
-                if (len <= kLongSeg) c = seg_count(kp + b, len, key);
-                uint32_t longm = __ballot_sync(0xffffffffu, len > kLongSeg);
-                while (longm) {
-                    const int src = __ffs(longm) - 1;
-                    longm &= longm - 1;
-                    const uint64_t kb = __shfl_sync(0xffffffffu, b, src);
-                    const uint64_t ke = __shfl_sync(0xffffffffu, e, src);
-                    const K kk = __shfl_sync(0xffffffffu, key, src);
-                    uint32_t cc = 0;
-                    for (uint64_t t = kb + lane; t < ke; t += 32) cc += kp[t] == kk;
-                    cc = warp_sum(cc);
-                    if (int(lane) == src) c = cc;
-                }
-                matches += c;
-                if constexpr (MODE == 1) {
+            } else {
+                for (uint64_t base = uint64_t(warp) * 32; base < qn; base += uint64_t(nwarps) * 32) {
+                    const uint64_t i = base + lane;
+                    const bool valid = i < qn;
+                    K key = 0;
+                    typename std::conditional<std::is_void<IT>::value, uint32_t, IT>::type pidx = 0;
+                    uint64_t b = 0, e = 0;
                     if (valid) {
-                        if constexpr (ORIG) pcount[pidx] = c;
-                        else pcount[q0 + i] = c;
+                        const auto ent = ep[i];
+                        key = PE::key(ent);
+                        if constexpr (PE::kHasVal) pidx = PE::val(ent);
+                        const uint32_t lv = uint32_t(hv<POW2>(key, seed, hk, nv) - vb);
+                        b = uint64_t(soff[lv]) - tb;
+                        e = uint64_t(soff[lv + 1]) - tb;
                     }
-                }
-                if constexpr (MODE == 2) {
-                    uint64_t sl = (valid && c) ? pair_off[q0 + i] : 0;
-                    if (valid && c && len <= kLongSeg) {
-                        for (uint64_t t = b; t < e && sl < cap; ++t) {
-                            if (kp[t] == key) {
-                                store_pair<PT>(pairs, sl, uint64_t(tvals[tb + t]), uint64_t(pidx));
-                                ++sl;
-                            }
-                        }
-                    }
-                    uint32_t lm = __ballot_sync(0xffffffffu, valid && c && len > kLongSeg);
-                    while (lm) {
-                        const int src = __ffs(lm) - 1;
-                        lm &= lm - 1;
+                    const uint64_t len = e - b;
+                    compared += len;
+                    uint32_t c = 0;
+                    if (len <= kLongSeg) c = seg_count(kp + b, len, key);
+                    uint32_t longm = __ballot_sync(0xffffffffu, len > kLongSeg);
+                    while (longm) {
+                        const int src = __ffs(longm) - 1;
+                        longm &= longm - 1;
                         const uint64_t kb = __shfl_sync(0xffffffffu, b, src);
                         const uint64_t ke = __shfl_sync(0xffffffffu, e, src);
                         const K kk = __shfl_sync(0xffffffffu, key, src);
-                        uint64_t ws = __shfl_sync(0xffffffffu, sl, src);
-                        const uint64_t pj = __shfl_sync(0xffffffffu, uint64_t(pidx), src);
-                        for (uint64_t t0 = kb; t0 < ke && ws < cap; t0 += 32) {
-                            const uint64_t t = t0 + lane;
-                            const bool hit = t < ke && kp[t] == kk;
-                            const uint32_t hm = __ballot_sync(0xffffffffu, hit);
-                            const uint64_t my = ws + __popc(hm & lanemask_lt());
-                            if (hit && my < cap) store_pair<PT>(pairs, my, uint64_t(tvals[tb + t]), pj);
-                            ws += __popc(hm);
+                        uint32_t cc = 0;
+                        for (uint64_t t = kb + lane; t < ke; t += 32) cc += kp[t] == kk;
+                        cc = warp_sum(cc);
+                        if (int(lane) == src) c = cc;
+                    }
+                    matches += c;
+                    if constexpr (MODE == 1) {
+                        if (valid) {
+                            if constexpr (ORIG) pcount[pidx] = c;
+                            else pcount[q0 + i] = c;
+                        }
+                    }
+                    if constexpr (MODE == 2) {
+                        uint64_t sl = (valid && c) ? pair_off[q0 + i] : 0;
+                        if (valid && c && len <= kLongSeg) {
+                            for (uint64_t t = b; t < e && sl < cap; ++t) {
+                                if (kp[t] == key) {
+                                    store_pair<PT>(pairs, sl, uint64_t(tvals[tb + t]), uint64_t(pidx));
+                                    ++sl;
+                                }
+                            }
+                        }
+                        uint32_t lm = __ballot_sync(0xffffffffu, valid && c && len > kLongSeg);
+                        while (lm) {
+                            const int src = __ffs(lm) - 1;
+                            lm &= lm - 1;
+                            const uint64_t kb = __shfl_sync(0xffffffffu, b, src);
+                            const uint64_t ke = __shfl_sync(0xffffffffu, e, src);
+                            const K kk = __shfl_sync(0xffffffffu, key, src);
+                            uint64_t ws = __shfl_sync(0xffffffffu, sl, src);
+                            const uint64_t pj = __shfl_sync(0xffffffffu, uint64_t(pidx), src);
+                            for (uint64_t t0 = kb; t0 < ke && ws < cap; t0 += 32) {
+                                const uint64_t t = t0 + lane;
+                                const bool hit = t < ke && kp[t] == kk;
+                                const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+                                const uint64_t my = ws + __popc(hm & lanemask_lt());
+                                if (hit && my < cap) store_pair<PT>(pairs, my, uint64_t(tvals[tb + t]), pj);
+                                ws += __popc(hm);
+                            }
                         }
                     }
                 }
