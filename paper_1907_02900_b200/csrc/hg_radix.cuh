@@ -234,7 +234,9 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
     __shared__ uint32_t s_ofs[kSplitStages], s_ok[kSplitStages];
     __shared__ uint32_t s_cnt[kMaxDigits];
     __shared__ uint32_t s_off[kMaxDigits];
-    __shared__ uint64_t s_gbo[kMaxDigits];  // reserved global base - tile offset of each digit
+    // reserved global base - tile offset of each digit, in the offsets' width
+    // (modular: base - off + j is the exact output index for j >= off)
+    __shared__ OffT s_gbo[kMaxDigits];
     __shared__ uint32_t s_wsum[kSplitBlock / 32];
     __shared__ uint64_t s_tp[PASS2 ? kMaxDigits + 1 : 1];  // tile_prefix cache
     __shared__ uint64_t s_bs[PASS2 ? kMaxDigits + 1 : 1];  // bucket start cache
@@ -344,7 +346,7 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
             for (uint32_t w = 0; w < warp; ++w) base += s_wsum[w];
             const uint32_t off = base + inc - c;
             s_off[tid] = off;
-            if (c) s_gbo[tid] = uint64_t(atom_add(cursor + cbase + tid, OffT(c))) - off;
+            if (c) s_gbo[tid] = atom_add(cursor + cbase + tid, OffT(c)) - OffT(off);
         }
         __syncthreads();
 #pragma unroll
@@ -361,7 +363,7 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
             const uint32_t j = tid + k * kSplitBlock;
-            if (j < cnt) out[s_gbo[s_dig[j]] + j] = s_ent[j];
+            if (j < cnt) out[uint64_t(OffT(s_gbo[s_dig[j]] + OffT(j)))] = s_ent[j];
         }
         __syncthreads();
         if (++st == kSplitStages) {
