@@ -464,31 +464,35 @@ __device__ __forceinline__ uint32_t pair_count(const K* __restrict__ kp, const P
                                                const OffT* soff, uint64_t i, uint64_t qn, uint64_t tb,
                                                uint64_t vb, uint64_t seed, int hk, const Divisor& nv,
                                                uint64_t& compared, K& key, uint64_t& b, uint64_t& e) {
+    // partition-relative positions in the offsets' width (u32 at C2)
+    using I = OffT;
     const uint32_t lane = threadIdx.x & 31;
-    b = e = 0;
+    I bi = 0, ei = 0;
     key = 0;
     if (i < qn) {
         key = PE::key(ent);
         const uint32_t lv = uint32_t(hv<POW2>(key, seed, hk, nv) - vb);
-        b = uint64_t(soff[lv]) - tb;
-        e = uint64_t(soff[lv + 1]) - tb;
+        bi = I(soff[lv]) - I(tb);
+        ei = I(soff[lv + 1]) - I(tb);
     }
-    const uint64_t len = e - b;
+    const I len = ei - bi;
     compared += len;
     uint32_t c = 0;
-    if (len <= kLongSeg) c = seg_count(kp + b, len, key);
-    uint32_t longm = __ballot_sync(0xffffffffu, len > kLongSeg);
+    if (len <= I(kLongSeg)) c = seg_count(kp + bi, uint64_t(len), key);
+    uint32_t longm = __ballot_sync(0xffffffffu, len > I(kLongSeg));
     while (longm) {
         const int src = __ffs(longm) - 1;
         longm &= longm - 1;
-        const uint64_t kb = __shfl_sync(0xffffffffu, b, src);
-        const uint64_t ke = __shfl_sync(0xffffffffu, e, src);
+        const I kb = __shfl_sync(0xffffffffu, bi, src);
+        const I ke = __shfl_sync(0xffffffffu, ei, src);
         const K kk = __shfl_sync(0xffffffffu, key, src);
         uint32_t cc = 0;
-        for (uint64_t t = kb + lane; t < ke; t += 32) cc += kp[t] == kk;
+        for (I t = kb + I(lane); t < ke; t += 32) cc += kp[t] == kk;
         cc = warp_sum(cc);
         if (int(lane) == src) c = cc;
     }
+    b = bi;
+    e = ei;
     return c;
 }
 
