@@ -139,32 +139,39 @@ k_part_hist(const K* __restrict__ keys, uint64_t n, uint64_t seed, int hk, Divis
     const uint64_t nvec = (n - head) / VEC;
     const V* body = reinterpret_cast<const V*>(keys + head);
     // two 16-byte vectors per step, software-pipelined one step ahead so the
-    // loads of step i+1 are in flight while step i's keys are counted
-    uint64_t q = gtid;
-    V a{}, b{};
-    if (q + stride < nvec) {
-        a = __ldcs(body + q);
-        b = __ldcs(body + q + stride);
-    }
-    for (; q + stride < nvec; q += 2 * stride) {
-        const V ca = a, cb = b;
-        if (q + 3 * stride < nvec) {
-            a = __ldcs(body + q + 2 * stride);
-            b = __ldcs(body + q + 3 * stride);
+    // loads of step i+1 are in flight while step i's keys are counted; vector
+    // indices in 32 bits whenever they fit
+    auto sweep = [&](auto idx_t) {
+        using I = decltype(idx_t);
+        const I nv_ = I(nvec), st = I(stride);
+        I q = I(gtid);
+        V a{}, b{};
+        if (q + st < nv_) {
+            a = __ldcs(body + q);
+            b = __ldcs(body + q + st);
         }
-        const K* ka = reinterpret_cast<const K*>(&ca);
-        const K* kb = reinterpret_cast<const K*>(&cb);
+        for (; q + st < nv_; q += 2 * st) {
+            const V ca = a, cb = b;
+            if (q + 3 * st < nv_) {
+                a = __ldcs(body + q + 2 * st);
+                b = __ldcs(body + q + 3 * st);
+            }
+            const K* ka = reinterpret_cast<const K*>(&ca);
+            const K* kb = reinterpret_cast<const K*>(&cb);
 #pragma unroll
-        for (int k = 0; k < VEC; ++k) count(ka[k]);
+            for (int k = 0; k < VEC; ++k) count(ka[k]);
 #pragma unroll
-        for (int k = 0; k < VEC; ++k) count(kb[k]);
-    }
-    if (q < nvec) {
-        const V a1 = __ldcs(body + q);
-        const K* ka = reinterpret_cast<const K*>(&a1);
+            for (int k = 0; k < VEC; ++k) count(kb[k]);
+        }
+        if (q < nv_) {
+            const V a1 = __ldcs(body + q);
+            const K* ka = reinterpret_cast<const K*>(&a1);
 #pragma unroll
-        for (int k = 0; k < VEC; ++k) count(ka[k]);
-    }
+            for (int k = 0; k < VEC; ++k) count(ka[k]);
+        }
+    };
+    if (nvec + 4 * stride < (uint64_t(1) << 32)) sweep(uint32_t(0));
+    else sweep(uint64_t(0));
     const uint64_t done = head + nvec * VEC;
     if (gtid < n - done) count(keys[done + gtid]);
     __syncthreads();
