@@ -17,7 +17,11 @@
 //   * hashers: VertexHasher and hashgraph::IdentityHasher (key % V) run on
 //     the device; any other VertexHashFn is rejected at compile time
 //     (a host functor cannot be evaluated by the kernels). Other hasher types
-//     opt in by specialising hashgraph::device_hasher<H>.
+//     opt in by specialising hashgraph::device_hasher<H> (kind + seed), e.g.
+//     the reference tests' support::IdentityHasher (tests/cpp/ref_prelude.hpp).
+//     The hasher passed to probe_standard / count_instances / validate_csr is
+//     the one used, exactly as in the reference (join.hpp:117-118,
+//     core.hpp:238, :271), not the table's.
 //   * the table lives in HBM; offsets()/edges() export it to host memory on
 //     first access (cached). Tables built from host vectors are uploaded on
 //     first device use.
@@ -357,12 +361,13 @@ inline HashGraph build_v2(std::span<const std::uint64_t> keys, const BuildConfig
     return build_v2(keys, cfg, VertexHasher{cfg.hash_seed}, stats, vertex_count);
 }
 
-// core.hpp:235-246
+// core.hpp:235-246: the key's vertex is hasher(key, V) for the hasher passed
 template <VertexHashFn H>
-std::uint64_t count_instances(const HashGraph& hg, std::uint64_t key, const H&) {
+std::uint64_t count_instances(const HashGraph& hg, std::uint64_t key, const H& hasher) {
     static_assert(device_hasher<H>::supported, "hasher has no device implementation");
     std::uint64_t c = 0;
-    detail::check(hg_count_instances(hg.device_table(), key, &c, nullptr));
+    detail::check(hg_count_instances_hasher(hg.device_table(), key, device_hasher<H>::kind,
+                                            device_hasher<H>::seed(hasher), &c, nullptr));
     return c;
 }
 
@@ -373,7 +378,7 @@ inline std::uint64_t count_instances(const HashGraph& hg, std::uint64_t key) {
 // core.hpp:251-287 (device validator; host-constructed tables are uploaded)
 template <VertexHashFn H>
 std::optional<std::string> validate_csr(const HashGraph& hg, std::uint64_t expected_entries,
-                                        const H&) {
+                                        const H& hasher) {
     static_assert(device_hasher<H>::supported, "hasher has no device implementation");
     static const char* const kWhat[] = {
         "", "table has no vertices", "offsets length is not num_vertices + 1",
@@ -384,7 +389,9 @@ std::optional<std::string> validate_csr(const HashGraph& hg, std::uint64_t expec
     if (hg.num_vertices() < 1) return std::string(kWhat[1]);
     int32_t code = 0;
     try {
-        detail::check(hg_validate(hg.device_table(), nullptr, expected_entries, &code, nullptr));
+        detail::check(hg_validate_hasher(hg.device_table(), nullptr, expected_entries,
+                                         device_hasher<H>::kind, device_hasher<H>::seed(hasher),
+                                         &code, nullptr));
     } catch (const std::invalid_argument&) {
         return std::string(kWhat[2]);
     }
@@ -418,10 +425,29 @@ struct JoinResult {
     std::optional<std::vector<MatchPair>> pairs;
 };
 
-// join.hpp:110-136
+namespace detail {
+// Host landing buffer for up to `cap` pairs: uninitialised storage (pages are
+// touched only by the pairs actually written), copied into the result vector.
+struct PairBuffer {
+    std::unique_ptr<unsigned char[]> raw;
+    std::uint64_t cap = 0;
+    void* reserve(std::uint64_t n) {
+        cap = n;
+        raw.reset(n ? new unsigned char[n * sizeof(MatchPair)] : nullptr);
+        return raw.get();
+    }
+    std::vector<MatchPair> take(std::uint64_t written) const {
+        const auto* p = reinterpret_cast<const MatchPair*>(raw.get());
+        return std::vector<MatchPair>(p, p + std::min(written, cap));
+    }
+};
+}  // namespace detail
+
+// join.hpp:110-136: every probe is hashed with the hasher passed
+// (join.hpp:117-118), the table's own by default (join.hpp:133-136)
 template <VertexHashFn H>
 JoinResult probe_standard(const HashGraph& hg, std::span<const std::uint64_t> probe_keys,
-                          const H&, const ProbeOptions& opts = {}) {
+                          const H& hasher, const ProbeOptions& opts = {}) {
     static_assert(device_hasher<H>::supported, "hasher has no device implementation");
     static_assert(sizeof(MatchPair) == 16, "MatchPair must match the C-ABI pair layout");
     hg_probe_options o;
@@ -429,12 +455,14 @@ JoinResult probe_standard(const HashGraph& hg, std::span<const std::uint64_t> pr
     o.materialize = opts.materialize ? 1 : 0;
     o.pair_width = 8;
     o.pair_cap = opts.pair_cap;
-    std::vector<MatchPair> pairs;
+    o.flags = HG_PROBE_HASHER;
+    o.hash_kind = device_hasher<H>::kind;
+    o.hash_seed = device_hasher<H>::seed(hasher);
+    detail::PairBuffer buf;
     if (opts.materialize) {
         const std::uint64_t bound = probe_keys.size() * std::max<std::uint64_t>(hg.num_edges(), 1);
-        pairs.resize(std::min<std::uint64_t>(opts.pair_cap, bound));
-        o.pairs = pairs.data();
-        if (pairs.empty()) o.pair_cap = 0;
+        o.pairs = buf.reserve(std::min<std::uint64_t>(opts.pair_cap, bound));
+        if (!o.pairs) o.pair_cap = 0;
     }
     hg_probe_result r{};
     detail::check(hg_probe(hg.device_table(), probe_keys.data(), 8, probe_keys.size(), &o, &r,
@@ -443,9 +471,8 @@ JoinResult probe_standard(const HashGraph& hg, std::span<const std::uint64_t> pr
     res.match_count = r.match_count;
     res.key_comparisons = r.key_comparisons;
     if (opts.materialize) {
-        pairs.resize(r.pairs_written);
         res.truncated = r.match_count > opts.pair_cap;
-        res.pairs = std::move(pairs);
+        res.pairs = buf.take(r.pairs_written);
     }
     return res;
 }
@@ -474,29 +501,27 @@ std::uint64_t intersect_adjacency(std::span<const Entry> a, std::span<const Entr
 
 namespace detail {
 inline JoinResult join_result(const hg_probe_result& r, const ProbeOptions& opts,
-                              std::vector<MatchPair>&& pairs) {
+                              const PairBuffer& buf) {
     JoinResult res;
     res.match_count = r.match_count;
     res.key_comparisons = r.key_comparisons;
     if (opts.materialize) {
-        pairs.resize(r.pairs_written);
         res.truncated = r.match_count > opts.pair_cap;
-        res.pairs = std::move(pairs);
+        res.pairs = buf.take(r.pairs_written);
     }
     return res;
 }
 
 inline hg_probe_options join_options(const ProbeOptions& opts, std::uint64_t bound,
-                                     std::vector<MatchPair>& pairs) {
+                                     PairBuffer& buf) {
     hg_probe_options o;
     hg_probe_options_init(&o);
     o.materialize = opts.materialize ? 1 : 0;
     o.pair_width = 8;
     o.pair_cap = opts.pair_cap;
     if (opts.materialize) {
-        pairs.resize(std::min<std::uint64_t>(opts.pair_cap, bound));
-        o.pairs = pairs.data();
-        if (pairs.empty()) o.pair_cap = 0;
+        o.pairs = buf.reserve(std::min<std::uint64_t>(opts.pair_cap, bound));
+        if (!o.pairs) o.pair_cap = 0;
     }
     return o;
 }
@@ -507,13 +532,13 @@ inline hg_probe_options join_options(const ProbeOptions& opts, std::uint64_t bou
 // index in B's input) in sequential order (vertex, A position, B position).
 inline JoinResult probe_new_prepared(const HashGraph& hg_a, const HashGraph& hg_b,
                                      const ProbeOptions& opts = {}) {
-    std::vector<MatchPair> pairs;
+    detail::PairBuffer pairs;
     const hg_probe_options o = detail::join_options(
         opts, std::max<std::uint64_t>(hg_a.num_edges(), 1) * std::max<std::uint64_t>(hg_b.num_edges(), 1),
         pairs);
     hg_probe_result r{};
     detail::check(hg_probe_new_prepared(hg_a.device_table(), hg_b.device_table(), &o, &r, nullptr));
-    return detail::join_result(r, opts, std::move(pairs));
+    return detail::join_result(r, opts, pairs);
 }
 
 // join.hpp:170-182: both inputs built (binned build) over the V of the
@@ -530,14 +555,14 @@ JoinResult probe_new(std::span<const std::uint64_t> keys_a, std::span<const std:
     c.hash_seed = device_hasher<H>::seed(hasher);
     c.hash_kind = device_hasher<H>::kind;
     c.stable = cfg.mode == ExecMode::sequential ? 1 : 0;
-    std::vector<MatchPair> pairs;
+    detail::PairBuffer pairs;
     const hg_probe_options o = detail::join_options(
         opts, std::max<std::uint64_t>(keys_a.size(), 1) * std::max<std::uint64_t>(keys_b.size(), 1),
         pairs);
     hg_probe_result r{};
     detail::check(hg_probe_new(keys_a.data(), keys_a.size(), keys_b.data(), keys_b.size(), 8, &c,
                                &o, &r, nullptr));
-    return detail::join_result(r, opts, std::move(pairs));
+    return detail::join_result(r, opts, pairs);
 }
 
 inline JoinResult probe_new(std::span<const std::uint64_t> keys_a,

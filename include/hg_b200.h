@@ -143,8 +143,22 @@ typedef struct hg_probe_options {
     uint64_t* device_result; /* nullable device u64[2] {match_count, key_comparisons}; when set
                                 the call is fully asynchronous (result is zeroed) */
     int32_t method;          /* 0 auto, 1 direct gathers, 2 vertex-range partitioned probes */
+    int32_t flags;           /* HG_PROBE_* bits below */
+    uint64_t hash_seed;      /* with HG_PROBE_HASHER: the probe-side hasher (join.hpp:110-131 */
+    int32_t hash_kind;       /*   hashes every probe with the caller's hasher, not the table's) */
     int32_t reserved;
 } hg_probe_options;
+
+/* hg_probe_options.flags: the pinned host probe buffer already holds its final
+ * contents when hg_probe is called (no earlier work on `stream` writes it), so
+ * its chunked host->device copies may start before earlier work on `stream`
+ * (e.g. the build of the probed table) has finished. Without it the copies
+ * are ordered after all earlier work on `stream`. */
+#define HG_PROBE_HOST_READY 1
+/* hg_probe_options.flags: hash the probes with (hash_kind, hash_seed) instead
+ * of the table's own hasher -- probe_standard(hg, keys, hasher, opts),
+ * join.hpp:110-131: vertex = hasher(key, V), then that vertex's segment. */
+#define HG_PROBE_HASHER 2
 
 void hg_probe_options_init(hg_probe_options* opts);
 
@@ -181,14 +195,26 @@ hg_status hg_probe_new(const void* keys_a, uint64_t na, const void* keys_b, uint
                        int32_t key_width, const hg_build_config* cfg, const hg_probe_options* opts,
                        hg_probe_result* result, void* stream);
 
-/* count_instances (core.hpp:235-246). */
+/* count_instances (core.hpp:235-246) with the table's own hasher. */
 hg_status hg_count_instances(const hg_table* t, uint64_t key, uint64_t* out, void* stream);
+
+/* count_instances(hg, key, hasher) (core.hpp:235-242): the key's vertex is
+ * hasher(key, V) for the hasher (hash_kind, hash_seed) the caller passes. */
+hg_status hg_count_instances_hasher(const hg_table* t, uint64_t key, int32_t hash_kind,
+                                    uint64_t hash_seed, uint64_t* out, void* stream);
 
 /* validate_csr (core.hpp:251-287) on the device, plus (input_keys != NULL)
  * the check keys[j] == input_keys[vals[j]]. *violation = 0 when valid, else
  * the code of the first violated invariant (see hg_util.cu). */
 hg_status hg_validate(const hg_table* t, const void* input_keys, uint64_t expected_entries,
                       int32_t* violation, void* stream);
+
+/* validate_csr(hg, expected, hasher) (core.hpp:251-282): as hg_validate, with
+ * the hash-consistency check (entry under hasher(key, V)) made with the
+ * caller's hasher (hash_kind, hash_seed). */
+hg_status hg_validate_hasher(const hg_table* t, const void* input_keys, uint64_t expected_entries,
+                             int32_t hash_kind, uint64_t hash_seed, int32_t* violation,
+                             void* stream);
 
 /* Multi-GPU routing (K11). Shard g of G owns global vertices
  * [g*S, min((g+1)*S, V)), S = ceil(V/G) (the reference's bin formula,

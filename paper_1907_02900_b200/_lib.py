@@ -57,6 +57,9 @@ class hg_probe_options(C.Structure):
         ("counts", C.c_void_p),
         ("device_result", C.c_void_p),
         ("method", C.c_int32),
+        ("flags", C.c_int32),
+        ("hash_seed", C.c_uint64),
+        ("hash_kind", C.c_int32),
         ("reserved", C.c_int32),
     ]
 
@@ -108,6 +111,8 @@ SIGNATURES = {
                             C.POINTER(hg_probe_options), C.POINTER(hg_probe_result), _vp]),
     "hg_count_instances": (_i32, [_vp, _u64, C.POINTER(_u64), _vp]),
     "hg_validate": (_i32, [_vp, _vp, _u64, C.POINTER(_i32), _vp]),
+    "hg_count_instances_hasher": (_i32, [_vp, _u64, _i32, _u64, C.POINTER(_u64), _vp]),
+    "hg_validate_hasher": (_i32, [_vp, _vp, _u64, _i32, _u64, C.POINTER(_i32), _vp]),
     "hg_generate": (_i32, [_vp, _i32, _u64, _i32, _u64, _u64, C.c_double, _vp, _u64, _vp]),
     "hg_shard_range": (_i32, [_u64, C.c_uint32, C.c_uint32, C.POINTER(_u64), C.POINTER(_u64)]),
     "hg_route": (_i32, [_vp, _i32, _vp, _i32, _u64, _u64, _u64, _i32, _u64, C.c_uint32, _vp, _vp,

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kBuildBlock)
 k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
              const OffT* __restrict__ part_start /* nparts + 1 partition offsets */,
              uint64_t nparts, uint64_t nv_total, uint64_t seed, int hk, Divisor nv,
-             uint32_t pshift, OffT* __restrict__ offs, K* __restrict__ okeys,
+             uint32_t pshift, uint64_t obase, OffT* __restrict__ offs, K* __restrict__ okeys,
              VT* __restrict__ ovals, uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_n) {
     using PE = EntryT<K, VT>;
     using E = typename PE::T;
@@ -155,7 +155,7 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
             // oversized (skewed) partition: built by the grid-wide K7b
             // kernels; here only its counters (offs[vb+1 .. vb+pv]) are zeroed
             for (uint32_t j = tid; j < pv; j += kBuildBlock) offs[vb + j + 1] = OffT(0);
-            if (p == 0 && tid == 0) offs[0] = 0;
+            if (p == 0 && tid == 0) offs[0] = OffT(obase);
             if (tid == 0) big_list[atomicAdd(big_n, 1u)] = uint32_t(p);
             __syncthreads();
             continue;
@@ -163,6 +163,7 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
         __syncthreads();
         // exclusive scan of cnt[0..pv): thread owns `per` consecutive counters
         // (vectorised 16-byte shared loads/stores when per is a multiple of 4)
+        const uint64_t so = s + obase;  // offsets are written with the table's entry base
         const uint32_t per = (pv + kBuildBlock - 1) / kBuildBlock;
         const uint32_t j0 = min(pv, tid * per), j1 = min(pv, j0 + per);
         const bool vec = (per & 3) == 0 && j1 - j0 == per && per <= 16;
@@ -206,10 +207,10 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
                 sts128(cnt + j0 + q, st);
                 const uint32_t nxt = st.w + c4.w;
                 if (!coal) {
-                    offs[vb + j0 + q + 1] = OffT(s + st.y);
-                    offs[vb + j0 + q + 2] = OffT(s + st.z);
-                    offs[vb + j0 + q + 3] = OffT(s + st.w);
-                    offs[vb + j0 + q + 4] = OffT(s + nxt);
+                    offs[vb + j0 + q + 1] = OffT(so + st.y);
+                    offs[vb + j0 + q + 2] = OffT(so + st.z);
+                    offs[vb + j0 + q + 3] = OffT(so + st.w);
+                    offs[vb + j0 + q + 4] = OffT(so + nxt);
                 }
                 acc = nxt;
             }
@@ -218,10 +219,10 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
                 const uint32_t c = cnt[j];
                 cnt[j] = acc;  // exclusive start
                 acc += c;
-                if (!coal) offs[vb + j + 1] = OffT(s + acc);  // end(j)
+                if (!coal) offs[vb + j + 1] = OffT(so + acc);  // end(j)
             }
         }
-        if (p == 0 && tid == 0) offs[0] = 0;
+        if (p == 0 && tid == 0) offs[0] = OffT(obase);
         // the previous partition's bulk stores must have read the staging arrays
         if (tid == 0) bulk_wait_read();
         __syncthreads();
@@ -232,8 +233,8 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
                 const uint4 st = lds128(cnt + 4 * c);
                 const uint32_t nxt = 4 * c + 4 < pv ? cnt[4 * c + 4] : cntp;
                 *reinterpret_cast<uint4*>(offs + vb + 4 * c + 1) =
-                    make_uint4(uint32_t(s) + st.y, uint32_t(s) + st.z, uint32_t(s) + st.w,
-                               uint32_t(s) + nxt);
+                    make_uint4(uint32_t(so) + st.y, uint32_t(so) + st.z, uint32_t(so) + st.w,
+                               uint32_t(so) + nxt);
             }
         }
         if (staged) {
@@ -259,390 +260,11 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
     if (tid == 0) bulk_wait_all();
 }
 
-// ---------------------------------------------------------------- K67 (fused)
-// Pass 2 of the partitioning (K6b) and the per-partition build (K7) in one
-// persistent kernel, so the partition-ordered entries travel through L2
-// instead of HBM. Tasks come from one atomic ticket in the order
-//   [pass-2 tiles of bucket 0][partitions of bucket 0][tiles of bucket 1]...
-// (bucket = one pass-1 digit = 2^b2 partitions, ~8 MB of entries at C2), so
-// at any time the grid works on about one bucket: its tiles scatter the
-// bucket's entries into `reorg`, and its partition tasks -- which wait for
-// the bucket's tile counter -- read them back while they are still in L2 and
-// then discard the lines (discard.global.L2: no write-back of dead data).
-// Thread 0 schedules: while the CTA processes task i, the TMA load of task
-// i+1 is already in flight into the other of two stage buffers (a partition
-// task whose bucket is not finished yet is loaded at the top of the next
-// iteration instead). A stage buffer holds a tile or a partition's entries;
-// after a partition's entries are in registers it is reused as the key /
-// value staging for that partition's TMA bulk stores.
-constexpr int kFuseBlock = 512;
-constexpr uint32_t kFuseLag = 1;  // buckets between a bucket's tiles and its partitions
-
-template <typename K, typename VT>
-struct FuseLayout {
-    using E = typename EntryT<K, VT>::T;
-    static constexpr int kTileItems = split_items<E>();
-    static constexpr uint32_t kTile = kFuseBlock * kTileItems;
-    static constexpr int kItems = 9;                        // partition entries per thread
-    // staged entries per partition: 1/16 above the 4096-entry partitions the
-    // geometry aims for (larger ones take the K7b path), so two CTAs fit an SM
-    static constexpr uint32_t kCap = 4096 + 256;
-    static_assert(kCap <= uint32_t(kFuseBlock) * kItems, "items per thread");
-    static constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
-    // stage: a tile, or a partition's entries and later its key staging
-    static constexpr size_t kStage =
-        align16(cmax(cmax(size_t(kTile) * sizeof(E), size_t(kCap) * sizeof(E)),
-                     size_t(kCap + 4) * sizeof(K)) + 32);
-    // region B: a tile's digit-sorted entries + digits, or a partition's
-    // vertex counters followed by its value staging
-    static size_t region_b(uint32_t P) {
-        return cmax(align16(size_t(kTile) * sizeof(E)) + align16(kTile),
-                    align16(size_t(P) * 4) + align16(size_t(kCap + 4) * sizeof(VT)));
-    }
-    static size_t bytes(uint32_t P) { return 2 * kStage + region_b(P); }
-};
-
-struct FuseTask {
-    uint64_t s, e;      // tile: entry range in mid; partition: entry range in reorg
-    uint64_t p;         // partition id (partition task)
-    uint32_t b;         // bucket
-    uint32_t kind;      // 0 none (past the end), 1 tile, 2 partition, 3 oversized partition
-    uint32_t ofs;       // byte offset of the data inside the stage buffer
-    uint32_t loaded;    // a TMA load was issued (the stage barrier will complete)
-};
-
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void discard_l2(const void* p) {
-    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
-}
-
-template <typename K, typename VT, typename OffT, int POW2>
-__global__ void __launch_bounds__(kFuseBlock, 2)
-k_split_build(const typename EntryT<K, VT>::T* __restrict__ mid, OffT* __restrict__ cur2,
-              const OffT* __restrict__ part_start, const uint64_t* __restrict__ tile_prefix,
-              uint32_t nb1, uint32_t b2, uint64_t nparts, uint64_t nv_total, uint64_t seed, int hk,
-              Divisor nv, uint32_t pshift, typename EntryT<K, VT>::T* __restrict__ reorg,
-              OffT* __restrict__ offs, K* __restrict__ okeys, VT* __restrict__ ovals,
-              uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_n,
-              uint32_t* __restrict__ ticket, uint32_t* __restrict__ done) {
-    using PE = EntryT<K, VT>;
-    using E = typename PE::T;
-    using L = FuseLayout<K, VT>;
-    constexpr int kItems = L::kItems;
-    constexpr int kTileItems = L::kTileItems;
-    constexpr uint32_t cap = L::kCap;
-    constexpr uint32_t KA = 16 / sizeof(K), VA = 16 / sizeof(VT);
-    extern __shared__ __align__(128) unsigned char smem[];
-    unsigned char* const stage0 = smem;
-    unsigned char* const regb = smem + 2 * L::kStage;
-    E* const s_ent = reinterpret_cast<E*>(regb);
-    uint8_t* const s_dig = regb + align16(size_t(L::kTile) * sizeof(E));
-    uint32_t* const cnt = reinterpret_cast<uint32_t*>(regb);
-    __shared__ uint64_t s_bar[2];
-    __shared__ FuseTask s_task[2];
-    __shared__ uint32_t s_ts[kMaxDigits + 1 + kFuseLag], s_tp[kMaxDigits + 1];
-    __shared__ OffT s_bs[kMaxDigits + 1];
-    __shared__ uint32_t s_cnt[kMaxDigits], s_off[kMaxDigits];
-    __shared__ OffT s_gbo[kMaxDigits];
-    __shared__ uint32_t s_wsum[kFuseBlock / 32];
-    __shared__ uint32_t s_defer;
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t P = 1u << pshift;
-    const uint32_t ndig = 1u << b2;
-    for (uint32_t b = tid; b <= nb1; b += kFuseBlock) {
-        const uint64_t q = (uint64_t(b) << b2) < nparts ? (uint64_t(b) << b2) : nparts;
-        s_tp[b] = tile_prefix[b];
-        s_bs[b] = part_start[q];
-    }
-    __syncthreads();
-    // Step k of the task sequence = [tiles of bucket k][partitions of bucket
-    // k - kLag]: a bucket's partitions are handed out one bucket after its
-    // tiles, so they rarely wait, while ~kLag + 1 buckets (~16 MB at C2) are
-    // live in L2. s_ts[k] = first task of step k.
-    const uint32_t nsteps = nb1 + kFuseLag;
-    if (tid == 0) {
-        uint64_t acc = 0;
-        for (uint32_t k = 0; k < nsteps; ++k) {
-            s_ts[k] = acc;
-            if (k < nb1) acc += s_tp[k + 1] - s_tp[k];
-            if (k >= kFuseLag) {
-                const uint64_t b = k - kFuseLag;
-                const uint64_t hi = ((b + 1) << b2) < nparts ? ((b + 1) << b2) : nparts;
-                acc += hi - (b << b2);
-            }
-        }
-        s_ts[nsteps] = acc;
-        mbar_init(&s_bar[0], 1);
-        mbar_init(&s_bar[1], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    // ---- scheduler helpers (thread 0)
-    auto decode = [&](uint64_t t, FuseTask& k) {
-        k.kind = 0;
-        k.loaded = 0;
-        if (t >= s_ts[nsteps]) return;
-        uint32_t lo = 0, hi = nsteps;
-        while (hi - lo > 1) {
-            const uint32_t m = (lo + hi) >> 1;
-            if (s_ts[m] <= t) lo = m; else hi = m;
-        }
-        const uint64_t r = t - s_ts[lo];
-        const uint64_t ntiles = lo < nb1 ? s_tp[lo + 1] - s_tp[lo] : 0;
-        if (r < ntiles) {
-            k.b = lo;
-            k.kind = 1;
-            k.s = s_bs[lo] + r * L::kTile;
-            k.e = s_bs[lo + 1] < k.s + L::kTile ? s_bs[lo + 1] : k.s + L::kTile;
-        } else {
-            k.b = lo - kFuseLag;
-            k.p = (uint64_t(k.b) << b2) + (r - ntiles);
-            k.s = part_start[k.p];
-            k.e = part_start[k.p + 1];
-            k.kind = k.e - k.s <= cap ? 2 : 3;
-        }
-    };
-    auto bucket_ready = [&](uint32_t b) { return ld_acquire_u32(done + b) >= uint32_t(s_tp[b + 1] - s_tp[b]); };
-    auto issue = [&](FuseTask& k, int st) {  // data load of a decoded task
-        if (k.kind == 1 || k.kind == 2) {
-            const E* src = k.kind == 1 ? mid + k.s : reorg + k.s;
-            fence_proxy_async();
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            k.ofs = tma_load_span(stage0 + st * L::kStage, src, uint32_t((k.e - k.s) * sizeof(E)),
-                                  &s_bar[st]);
-            k.loaded = 1;
-        }
-    };
-
-    if (tid == 0) {
-        FuseTask k;
-        decode(atomicAdd(ticket, 1u), k);
-        if (k.kind == 2)
-            while (!bucket_ready(k.b)) __nanosleep(200);
-        issue(k, 0);
-        s_task[0] = k;
-        s_defer = 0;
-    }
-    uint32_t ph[2] = {0, 0};
-    for (uint32_t it = 0;; ++it) {
-        const int st = int(it & 1);
-        __syncthreads();  // s_task[st] published; previous task fully done
-        FuseTask cur = s_task[st];
-        if (cur.kind == 0) break;
-        if (tid == 0 && s_defer) {
-            // deferred load of this partition task: its bucket is finishing
-            while (!bucket_ready(cur.b)) __nanosleep(100);
-            issue(cur, st);
-            s_task[st] = cur;
-            s_defer = 0;
-        }
-        if (tid == 0) {
-            // next task: load it now into the other stage unless it must wait
-            bulk_wait_read();  // earlier bulk stores no longer read that buffer
-            FuseTask nk;
-            decode(atomicAdd(ticket, 1u), nk);
-            if (nk.kind == 2 && !bucket_ready(nk.b)) {
-                s_defer = 1;
-            } else {
-                issue(nk, st ^ 1);
-            }
-            s_task[st ^ 1] = nk;
-        }
-        __syncthreads();
-        cur = s_task[st];
-        const unsigned char* const sbuf = stage0 + st * L::kStage;
-        if (cur.loaded) {
-            mbar_wait(&s_bar[st], ph[st]);
-            ph[st] ^= 1;
-        }
-        if (cur.kind == 1) {
-            // ---------------- pass-2 tile: split by the low digit
-            const E* src = reinterpret_cast<const E*>(sbuf + cur.ofs);
-            const uint32_t n_t = uint32_t(cur.e - cur.s);
-            const uint64_t cbase = uint64_t(cur.b) << b2;
-            for (uint32_t d = tid; d < ndig; d += kFuseBlock) s_cnt[d] = 0;
-            __syncthreads();
-            E ent[kTileItems];
-            uint32_t dr[kTileItems];
-#pragma unroll
-            for (int k = 0; k < kTileItems; ++k) {
-                const uint32_t j = tid + k * kFuseBlock;
-                if (j < n_t) {
-                    ent[k] = src[j];
-                    const uint32_t pp = uint32_t(hv<POW2>(PE::key(ent[k]), seed, hk, nv) >> pshift);
-                    const uint32_t d = pp & (ndig - 1);
-                    dr[k] = (d << 16) | atomicAdd(s_cnt + d, 1u);
-                }
-            }
-            __syncthreads();
-            const uint32_t c = tid < ndig ? s_cnt[tid] : 0;
-            uint32_t inc = c;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
-                if (int(lane) >= d) inc += y;
-            }
-            if (lane == 31) s_wsum[warp] = inc;
-            __syncthreads();
-            if (tid < ndig) {
-                uint32_t base = 0;
-                for (uint32_t w = 0; w < warp; ++w) base += s_wsum[w];
-                const uint32_t off = base + inc - c;
-                s_off[tid] = off;
-                if (c) s_gbo[tid] = atom_add(cur2 + cbase + tid, OffT(c)) - OffT(off);
-            }
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < kTileItems; ++k) {
-                const uint32_t j = tid + k * kFuseBlock;
-                if (j < n_t) {
-                    const uint32_t d = dr[k] >> 16;
-                    const uint32_t slot = s_off[d] + (dr[k] & 0xFFFFu);
-                    s_ent[slot] = ent[k];
-                    s_dig[slot] = uint8_t(d);
-                }
-            }
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < kTileItems; ++k) {
-                const uint32_t j = tid + k * kFuseBlock;
-                if (j < n_t) reorg[uint64_t(s_gbo[s_dig[j]]) + j] = s_ent[j];
-            }
-            // publish the tile: the barrier orders every thread's stores before
-            // thread 0's (cumulative) fence and the counter increment
-            __syncthreads();
-            if (tid == 0) {
-                __threadfence();
-                atomicAdd(done + cur.b, 1u);
-            }
-        } else if (cur.kind == 3) {
-            // ---------------- oversized partition: queued for the K7b kernels
-            const uint64_t vb = cur.p << pshift;
-            const uint32_t pv = uint32_t(nv_total - vb < P ? nv_total - vb : uint64_t(P));
-            for (uint32_t j = tid; j < pv; j += kFuseBlock) offs[vb + j + 1] = OffT(0);
-            if (cur.p == 0 && tid == 0) offs[0] = 0;
-            if (tid == 0) big_list[atomicAdd(big_n, 1u)] = uint32_t(cur.p);
-        } else {
-            // ---------------- partition build (K7 logic)
-            const uint64_t s = cur.s;
-            const uint32_t cntp = uint32_t(cur.e - cur.s);
-            const uint64_t vb = cur.p << pshift;
-            const uint32_t pv = uint32_t(nv_total - vb < P ? nv_total - vb : uint64_t(P));
-            for (uint32_t j = tid; j < pv; j += kFuseBlock) cnt[j] = 0;
-            const E* src = reinterpret_cast<const E*>(sbuf + cur.ofs);
-            E ent[kItems];
-#pragma unroll
-            for (int k = 0; k < kItems; ++k) {
-                const uint32_t i = tid + k * kFuseBlock;
-                if (i < cntp) ent[k] = src[i];
-            }
-            __syncthreads();  // counters zeroed; stage data in registers
-            // the partition's reorg lines are dead now: drop them from L2
-            {
-                const uintptr_t a0 = reinterpret_cast<uintptr_t>(reorg + s);
-                const uintptr_t a1 = reinterpret_cast<uintptr_t>(reorg + cur.e);
-                const uintptr_t l0 = (a0 + 127) & ~uintptr_t(127), l1 = a1 & ~uintptr_t(127);
-                for (uintptr_t a = l0 + uintptr_t(tid) * 128; a + 128 <= l1; a += uintptr_t(kFuseBlock) * 128)
-                    discard_l2(reinterpret_cast<const void*>(a));
-            }
-            uint32_t lr[kItems];
-#pragma unroll
-            for (int k = 0; k < kItems; ++k) {
-                const uint32_t i = tid + k * kFuseBlock;
-                if (i < cntp) {
-                    const uint32_t lv = uint32_t(hv<POW2>(PE::key(ent[k]), seed, hk, nv) - vb);
-                    lr[k] = (lv << 16) | atomicAdd(cnt + lv, 1u);
-                }
-            }
-            __syncthreads();
-            const uint32_t per = (pv + kFuseBlock - 1) / kFuseBlock;
-            const uint32_t j0 = min(pv, tid * per), j1 = min(pv, j0 + per);
-            const bool vec = (per & 3) == 0 && j1 - j0 == per && per <= 16;
-            uint32_t run = 0;
-            if (vec) {
-                for (uint32_t q = 0; q < per; q += 4) {
-                    const uint4 c4 = lds128(cnt + j0 + q);
-                    run += c4.x + c4.y + c4.z + c4.w;
-                }
-            } else {
-                for (uint32_t j = j0; j < j1; ++j) run += cnt[j];
-            }
-            uint32_t inc = run;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
-                if (int(lane) >= d) inc += y;
-            }
-            if (lane == 31) s_wsum[warp] = inc;
-            __syncthreads();
-            if (warp == 0) {
-                const uint32_t w = lane < kFuseBlock / 32 ? s_wsum[lane] : 0;
-                uint32_t wi = w;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, wi, d);
-                    if (int(lane) >= d) wi += y;
-                }
-                if (lane < kFuseBlock / 32) s_wsum[lane] = wi - w;
-            }
-            __syncthreads();
-            uint32_t acc = s_wsum[warp] + inc - run;
-            if (vec) {
-                for (uint32_t q = 0; q < per; q += 4) {
-                    const uint4 c4 = lds128(cnt + j0 + q);
-                    const uint4 stv = make_uint4(acc, acc + c4.x, acc + c4.x + c4.y,
-                                                 acc + c4.x + c4.y + c4.z);
-                    sts128(cnt + j0 + q, stv);
-                    const uint32_t nxt = stv.w + c4.w;
-                    if constexpr (sizeof(OffT) == 4) {
-                        *reinterpret_cast<uint4*>(offs + vb + j0 + q + 1) =
-                            make_uint4(uint32_t(s) + stv.y, uint32_t(s) + stv.z, uint32_t(s) + stv.w,
-                                       uint32_t(s) + nxt);
-                    } else {
-                        offs[vb + j0 + q + 1] = OffT(s + stv.y);
-                        offs[vb + j0 + q + 2] = OffT(s + stv.z);
-                        offs[vb + j0 + q + 3] = OffT(s + stv.w);
-                        offs[vb + j0 + q + 4] = OffT(s + nxt);
-                    }
-                    acc = nxt;
-                }
-            } else {
-                for (uint32_t j = j0; j < j1; ++j) {
-                    const uint32_t c = cnt[j];
-                    cnt[j] = acc;
-                    acc += c;
-                    offs[vb + j + 1] = OffT(s + acc);
-                }
-            }
-            if (cur.p == 0 && tid == 0) offs[0] = 0;
-            __syncthreads();
-            // key / value staging in this stage buffer (its entries are in registers)
-            unsigned char* const stg = stage0 + st * L::kStage;
-            K* skp = reinterpret_cast<K*>(stg) + (s & (KA - 1));
-            VT* svp = reinterpret_cast<VT*>(regb + align16(size_t(P) * 4)) + (s & (VA - 1));
-#pragma unroll
-            for (int k = 0; k < kItems; ++k) {
-                const uint32_t i = tid + k * kFuseBlock;
-                if (i < cntp) {
-                    const uint32_t pos = cnt[lr[k] >> 16] + (lr[k] & 0xFFFFu);
-                    skp[pos] = PE::key(ent[k]);
-                    svp[pos] = PE::val(ent[k]);
-                }
-            }
-            fence_proxy_async();
-            __syncthreads();
-            const bool x = bulk_store_span(okeys + s, skp, cntp, tid, kFuseBlock);
-            const bool y = bulk_store_span(ovals + s, svp, cntp, tid, kFuseBlock);
-            if (x || y) bulk_commit();
-        }
-    }
-    if (tid == 0) bulk_wait_all();
+template <typename OffT>
+__global__ void k_fill_offs(OffT* __restrict__ offs, uint64_t n, OffT v) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        offs[i] = v;
 }
 
 // ---------------------------------------------------------------- K7b
@@ -790,7 +412,7 @@ k7b_pass(const typename EntryT<K, VT>::T* __restrict__ reorg, const OffT* __rest
 template <typename OffT>
 __global__ void __launch_bounds__(1024)
 k7b_scan(const OffT* __restrict__ part_start, const uint32_t* __restrict__ list,
-         const uint32_t* __restrict__ big_n, uint64_t nv_total, uint32_t pshift,
+         const uint32_t* __restrict__ big_n, uint64_t nv_total, uint32_t pshift, uint64_t obase,
          OffT* __restrict__ offs) {
     __shared__ uint64_t s_warp[32];
     __shared__ uint64_t s_carry, s_tot;
@@ -801,7 +423,7 @@ k7b_scan(const OffT* __restrict__ part_start, const uint32_t* __restrict__ list,
         const uint64_t vb = p << pshift;
         const uint64_t P = uint64_t(1) << pshift;
         const uint64_t pv = nv_total - vb < P ? nv_total - vb : P;
-        if (threadIdx.x == 0) s_carry = part_start[p];
+        if (threadIdx.x == 0) s_carry = part_start[p] + obase;
         __syncthreads();
         for (uint64_t j0 = 0; j0 < pv; j0 += blockDim.x) {
             const uint64_t j = j0 + threadIdx.x;
@@ -841,7 +463,12 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
     const Divisor nv = make_divisor(global_nv(t), t.vbase);
     OffT* offs = static_cast<OffT*>(t.offs);
     cudaError_t e;
-    if (t.n == 0) return cudaMemsetAsync(offs, 0, (t.nv + 1) * sizeof(OffT), s);
+    if (t.n == 0) {
+        if (t.obase == 0) return cudaMemsetAsync(offs, 0, (t.nv + 1) * sizeof(OffT), s);
+        k_fill_offs<OffT><<<unsigned(std::min<uint64_t>((t.nv + 256) / 256, 4096)), 256, 0, s>>>(
+            offs, t.nv + 1, OffT(t.obase));
+        return cudaGetLastError();
+    }
 
     int dev = 0;
     cudaGetDevice(&dev);
@@ -870,43 +497,13 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
     uint32_t* big_list = reinterpret_cast<uint32_t*>(scratch + ps_bytes + pscr + reorg_bytes);
     uint64_t* big_pref = reinterpret_cast<uint64_t*>(scratch + ps_bytes + pscr + reorg_bytes + list_bytes);
     uint32_t* ticket = reinterpret_cast<uint32_t*>(scratch + ps_bytes + pscr + reorg_bytes + list_bytes +
-                                                   pref_bytes);  // ticket, big_n, done[kMaxDigits + 1]
+                                                   pref_bytes);  // ticket, big_n
     do {
-        if ((e = cudaMemsetAsync(ticket, 0, 8 + 4 * (kMaxDigits + 1), s)) != cudaSuccess)
-            break;  // ticket, big_n, per-bucket tile counters
-        // Opt-in (HG_FUSE=1): pass 2 + K7 fused (K67) for 8-byte entries with two
-        // radix passes. It moves 4 GB less DRAM traffic at C2 but, limited to
-        // two CTAs per SM with a one-task prefetch, measured 3.78 ms against
-        // 2.6 ms for K6b + K7, so it is not the default.
-        const bool fuse = sizeof(E) == 8 && g.b2 > 0 && getenv("HG_FUSE") &&
-                          getenv("HG_FUSE")[0] == '1';
-        Pass2State<K, VT, OffT> p2;
+        if ((e = cudaMemsetAsync(ticket, 0, 8, s)) != cudaSuccess) break;  // ticket, big_n
         e = partition<K, VT, OffT, POW2>(static_cast<const K*>(a.keys),
                                          static_cast<const VT*>(a.vals), t.n, t.seed, t.hash_kind,
-                                         nv, g, part_start, pscratch, reorg, s, kBuildPassNames,
-                                         fuse ? &p2 : nullptr);
+                                         nv, g, part_start, pscratch, reorg, s, kBuildPassNames);
         if (e != cudaSuccess) break;
-        if (fuse) {
-            using FL = FuseLayout<K, VT>;
-            auto kf = k_split_build<K, VT, OffT, POW2>;
-            const size_t fsm = FL::bytes(1u << g.pshift);
-            if ((e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(fsm))) != cudaSuccess)
-                break;
-            int per_sm = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, kFuseBlock, fsm);
-            const unsigned gf = unsigned(std::max(1, per_sm) * num_sms());
-            uint32_t* done = ticket + 2;
-            HG_LAUNCH("k67_split_build", s,
-                      kf<<<gf, kFuseBlock, fsm, s>>>(p2.mid, p2.cur2, part_start, p2.tile_prefix,
-                                                     p2.nb1, g.b2, g.nparts, t.nv, t.seed,
-                                                     t.hash_kind, nv, g.pshift, reorg, offs,
-                                                     static_cast<K*>(t.keys),
-                                                     static_cast<VT*>(t.vals), big_list, ticket + 1,
-                                                     ticket, done));
-            if ((e = cudaGetLastError()) != cudaSuccess) break;
-        }
-        if (!fuse) {
         auto kb = k_part_build<K, VT, OffT, POW2>;
         if ((e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(smem))) != cudaSuccess)
@@ -917,12 +514,11 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
             std::min<uint64_t>(uint64_t(std::max(1, per_sm)) * num_sms(), g.nparts));
         HG_LAUNCH("k7_part_build", s,
                   kb<<<gk, kBuildBlock, smem, s>>>(reorg, part_start, g.nparts, t.nv, t.seed,
-                                                   t.hash_kind, nv, g.pshift, offs,
+                                                   t.hash_kind, nv, g.pshift, t.obase, offs,
                                                    static_cast<K*>(t.keys),
                                                    static_cast<VT*>(t.vals), big_list,
                                                    ticket + 1));
         if ((e = cudaGetLastError()) != cudaSuccess) break;
-        }
         // oversized partitions (device-side count; the kernels exit at once
         // when there are none)
         uint32_t* big_n = ticket + 1;
@@ -948,11 +544,11 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
             HG_LAUNCH("k7b_big_scan", s,
                       (k7b_scan<OffT><<<unsigned(num_sms() * 2), 1024, 0, s>>>(part_start, big_list,
                                                                            big_n, t.nv, g.pshift,
-                                                                           offs)));
+                                                                           t.obase, offs)));
             HG_LAUNCH("k7b_big_place", s,
                       (kc1<<<gc, 512, hsm, s>>>(reorg, part_start, big_list, big_n, big_cpref, t.nv,
-                                               t.seed, nv, g.pshift, offs, static_cast<K*>(t.keys),
-                                               static_cast<VT*>(t.vals))));
+                                               t.seed, nv, g.pshift, offs, static_cast<K*>(t.keys) - t.obase,
+                                               static_cast<VT*>(t.vals) - t.obase)));
             e = cudaGetLastError();
             break;
         }
@@ -963,11 +559,11 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
         HG_LAUNCH("k7b_big_scan", s,
                   (k7b_scan<OffT><<<unsigned(num_sms() * 2), 1024, 0, s>>>(part_start, big_list,
                                                                        big_n, t.nv, g.pshift,
-                                                                       offs)));
+                                                                       t.obase, offs)));
         HG_LAUNCH("k7b_big_place", s,
                   (k7b_pass<K, VT, OffT, POW2, true><<<gb, 256, 0, s>>>(
                       reorg, part_start, big_list, big_n, big_pref, t.seed, nv, g.pshift, offs,
-                      static_cast<K*>(t.keys), static_cast<VT*>(t.vals))));
+                      static_cast<K*>(t.keys) - t.obase, static_cast<VT*>(t.vals) - t.obase)));
         e = cudaGetLastError();
     } while (false);
     cudaFreeAsync(scratch, s);

@@ -21,6 +21,7 @@
 
 #include "hg_common.cuh"
 #include "hg_internal.h"
+#include "hg_radix.cuh"
 #include "hg_scan.cuh"
 
 namespace hg {
@@ -34,6 +35,17 @@ int num_sms() {
         if (sms <= 0) sms = 148;
     }
     return sms;
+}
+
+size_t smem_optin() {
+    static int bytes = 0;
+    if (!bytes) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&bytes, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        if (bytes <= 0) bytes = 227 * 1024;
+    }
+    return size_t(bytes);
 }
 
 template <typename Kern>
@@ -281,10 +293,85 @@ static cudaError_t build_v1_impl(const TableDesc& t, const BuildArgs& a, cudaStr
 template <typename K, typename VT, typename OffT, int POW2>
 cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s);
 
+// Width (log2 vertices) of the slices a binned build is split into, 0 when
+// the whole vertex range fits 2^16 partitions of the tuned width (~4096
+// entries, 2048 for 16-byte entries; make_geom in hg_radix.cuh).
+static uint32_t v2_slice_shift(const TableDesc& t, const BuildArgs& a, size_t entry_bytes) {
+    if (t.n == 0) return 0;
+    const double target = entry_bytes >= 16 ? 2048.0 : 4096.0;
+    uint32_t ps = 0;
+    if (a.partition_vertices) {
+        ps = ceil_log2(a.partition_vertices);
+        if (ps > kMaxPartShift) ps = kMaxPartShift;
+    } else {
+        const double per_vertex = double(t.n) / double(t.nv);
+        while (ps < kMaxPartShift && per_vertex * double(uint64_t(2) << ps) <= target) ++ps;
+    }
+    return ceil_log2(t.nv) > 16 + ps ? 16 + ps : 0;
+}
+
+// Binned build over a vertex range wider than 2^16 partitions of the tuned
+// width (V > 2^28 at load 1, e.g. 2^31 keys or C5's 2^31-vertex shards). The
+// reference's bin split (core.hpp:192-197) is applied once more on top: K11
+// routes the keys into G slices of 2^sshift consecutive vertices (SoA keys +
+// input positions, hg_shard.cu), then each slice is built by the binned build
+// into its range of the one table -- offsets written with the slice's entry
+// base (TableDesc::obase), keys / values at the slice's entry range -- so
+// every slice keeps the tuned partition geometry (two 8-bit digits, K7 at two
+// CTAs per SM). Extra traffic: one routing pass, N (kb + vb) read + written.
+template <typename K, typename VT, typename OffT, int HM>
+static cudaError_t build_v2_sliced(const TableDesc& t, const BuildArgs& a, uint32_t sshift,
+                                   cudaStream_t s) {
+    const uint64_t S = uint64_t(1) << sshift;
+    const uint64_t G = (t.nv + S - 1) / S;
+    if (G > 256) return cudaErrorInvalidValue;
+    const size_t kbytes = (t.n * sizeof(K) + 255) & ~size_t(255);
+    const size_t vbytes = (t.n * sizeof(VT) + 255) & ~size_t(255);
+    char* scratch = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), kbytes + vbytes + 256 * 8, s);
+    if (e != cudaSuccess) return e;
+    K* rk = reinterpret_cast<K*>(scratch);
+    VT* rv = reinterpret_cast<VT*>(scratch + kbytes);
+    uint64_t* dcnt = reinterpret_cast<uint64_t*>(scratch + kbytes + vbytes);
+    uint64_t cnt[256];
+    do {
+        if ((e = route_keys(a.keys, sizeof(K), a.vals, sizeof(VT), t.n, 0, t.seed, t.hash_kind,
+                            global_nv(t), t.vbase, t.nv, S, uint32_t(G), rk, rv, dcnt, s)) !=
+            cudaSuccess)
+            break;
+        if ((e = cudaMemcpyAsync(cnt, dcnt, G * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+            (e = cudaStreamSynchronize(s)) != cudaSuccess)
+            break;
+        uint64_t start = 0;
+        for (uint64_t g = 0; g < G && e == cudaSuccess; ++g) {
+            TableDesc sub = t;
+            sub.nv = t.nv - g * S < S ? t.nv - g * S : S;
+            sub.n = cnt[g];
+            sub.gnv = global_nv(t);
+            sub.vbase = t.vbase + g * S;
+            sub.obase = t.obase + start;
+            sub.offs = static_cast<OffT*>(t.offs) + g * S;
+            sub.keys = static_cast<K*>(t.keys) + start;
+            sub.vals = static_cast<VT*>(t.vals) + start;
+            BuildArgs sa = a;
+            sa.keys = rk + start;
+            sa.vals = rv + start;
+            sa.n = cnt[g];
+            sa.stable = 0;
+            e = build_v2_impl<K, VT, OffT, HM>(sub, sa, s);
+            start += cnt[g];
+        }
+    } while (false);
+    cudaFreeAsync(scratch, s);
+    return e;
+}
+
 template <typename K, typename VT, typename OffT>
 static cudaError_t build_typed(const TableDesc& t, const BuildArgs& a, cudaStream_t s) {
+    const uint32_t sshift = a.variant == 2 ? v2_slice_shift(t, a, sizeof(typename EntryT<K, VT>::T)) : 0;
     cudaError_t e = dispatch_hash_mode(hash_mode(global_nv(t), t.hash_kind), [&](auto hm) {
         constexpr int HM = decltype(hm)::value;
+        if (sshift) return build_v2_sliced<K, VT, OffT, HM>(t, a, sshift, s);
         return a.variant == 2 ? build_v2_impl<K, VT, OffT, HM>(t, a, s)
                               : build_v1_impl<K, VT, OffT, HM>(t, a, s);
     });

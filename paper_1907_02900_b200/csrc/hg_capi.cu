@@ -237,10 +237,6 @@ hg_status hg_build(const void* keys, int32_t key_width, const void* vals, int32_
         hg_status st = hg_derived_vertex_count(n, cfg.load_factor, &nv);
         if (st != HG_OK) return st;
     }
-    if (cfg.variant == HG_BUILD_BINNED && nv > (uint64_t(1) << 30))
-        return fail(HG_EUNSUPPORTED,
-                    "binned build supports up to 2^30 vertices per device (two 8-bit partition "
-                    "digits); shard the table by hash range or use the simple build");
     int dev = 0;
     if (hg_status st = need_device(&dev); st != HG_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -397,12 +393,23 @@ hg_status hg_probe(const hg_table* t, const void* probes, int32_t probe_width, u
     if (opts.materialize && opts.pair_cap && !opts.pairs)
         return fail(HG_EINVAL, "materialize requires a pairs buffer");
     if (!opts.device_result && !result) return fail(HG_EINVAL, "result is NULL");
+    if ((opts.flags & HG_PROBE_HASHER) && opts.hash_kind != HG_HASH_MIX64 &&
+        opts.hash_kind != HG_HASH_IDENTITY)
+        return fail(HG_EINVAL, "unknown hash_kind");
     if (cudaSetDevice(t->device) != cudaSuccess) return fail(HG_ECUDA, "cudaSetDevice failed");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // the table as the probe sees it: join.hpp:117-118 hashes each probe with
+    // the caller's hasher (default: the table's own, join.hpp:133-136)
+    hg::TableDesc td = t->d;
+    if (opts.flags & HG_PROBE_HASHER) {
+        td.hash_kind = opts.hash_kind;
+        td.seed = opts.hash_seed;
+    }
 
     // Pinned host probes without pairs: chunked pipeline, each chunk's H2D
-    // copy (on a side stream) overlaps the previous chunk's probe kernels and
-    // whatever is still running on `stream` (e.g. the build of this table).
+    // copy (on a side stream) overlaps the previous chunk's probe kernels --
+    // and, with HG_PROBE_HOST_READY, whatever is still running on `stream`
+    // (e.g. the build of this table).
     constexpr uint64_t kPipeChunk = uint64_t(1) << 26;
     const bool pipelined = m >= 2 * kPipeChunk && !opts.materialize &&
                            probe_width == t->d.key_bytes && is_pinned_host(probes);
@@ -425,6 +432,33 @@ hg_status hg_probe(const hg_table* t, const void* probes, int32_t probe_width, u
     const bool want_pairs = opts.materialize && opts.pair_cap > 0;
     const bool counts_dev = opts.counts && is_device_ptr(opts.counts);
     const bool pairs_dev = want_pairs && is_device_ptr(opts.pairs);
+    // Host pair destination: the device staging is sized from the exact match
+    // count (one count-only pass first) instead of pair_cap, which defaults to
+    // 2^24 pairs (join.hpp:27) however few matches there are.
+    uint64_t cap_eff = opts.pair_cap;
+    if (want_pairs && !pairs_dev && m) {
+        uint64_t* dt = nullptr;
+        uint64_t ht[2] = {0, 0};
+        e = cudaMallocAsync(reinterpret_cast<void**>(&dt), 16, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(dt, 0, 16, s);
+        if (e == cudaSuccess) {
+            hg::ProbeArgs c;
+            c.probes = dprobes;
+            c.m = m;
+            c.totals = dt;
+            c.method = opts.method;
+            e = hg::probe_table(td, c, s);
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync(ht, dt, 16, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (dt) cudaFreeAsync(dt, s);
+        if (e != cudaSuccess) {
+            pin.release(s);
+            if (widened) cudaFreeAsync(widened, s);
+            return cuda_fail(e, "hg_probe: match count");
+        }
+        cap_eff = std::max<uint64_t>(1, std::min(opts.pair_cap, ht[0]));
+    }
     // scratch: totals[3] | counts[m] (if needed) | pair_offsets[m+1] | pairs staging
     uint64_t* totals = opts.device_result;
     void* scratch = nullptr;
@@ -436,7 +470,7 @@ hg_status hg_probe(const hg_table* t, const void* probes, int32_t probe_width, u
     const size_t po_off = cnt_off + cnt_bytes;
     const size_t po_bytes = opts.materialize ? (((m + 1) * 8 + 255) & ~size_t(255)) : 0;
     const size_t pr_off = po_off + po_bytes;
-    const size_t pr_bytes = (want_pairs && !pairs_dev) ? opts.pair_cap * 2 * opts.pair_width : 0;
+    const size_t pr_bytes = (want_pairs && !pairs_dev) ? cap_eff * 2 * opts.pair_width : 0;
     need = pr_off + pr_bytes;
     if (need && (e = cudaMallocAsync(&scratch, need, s)) != cudaSuccess) {
         pin.release(s);
@@ -459,10 +493,10 @@ hg_status hg_probe(const hg_table* t, const void* probes, int32_t probe_width, u
     a.totals = totals;
     a.pairs = pairs;
     a.pair_bytes = opts.pair_width;
-    a.cap = want_pairs ? opts.pair_cap : 0;
+    a.cap = want_pairs ? cap_eff : 0;
     a.pair_offsets = pair_off;
     a.method = opts.method;
-    if (e == cudaSuccess && !pipelined) e = hg::probe_table(t->d, a, s);
+    if (e == cudaSuccess && !pipelined) e = hg::probe_table(td, a, s);
     if (e == cudaSuccess && pipelined) {
         void* ring = nullptr;
         cudaStream_t cs = nullptr;
@@ -471,12 +505,18 @@ hg_status hg_probe(const hg_table* t, const void* probes, int32_t probe_width, u
         // the ring is allocated on the copy stream, so the first copies do not
         // wait for earlier work on `stream` (e.g. the build of this table)
         e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+        if (e == cudaSuccess && !(opts.flags & HG_PROBE_HOST_READY)) {
+            // stream order: the copies wait for everything enqueued on `stream`
+            // so far (which may still be writing the host buffer)
+            e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventRecord(ready, s);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ready, 0);
+        }
         if (e == cudaSuccess) e = cudaMallocAsync(&ring, 2 * cb, cs);
         for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
             e = cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming);
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming);
         }
-        (void)ready;
         const char* host = static_cast<const char*>(probes);
         for (uint64_t c = 0; e == cudaSuccess && c * kPipeChunk < m; ++c) {
             const int b = int(c & 1);
@@ -493,7 +533,7 @@ hg_status hg_probe(const hg_table* t, const void* probes, int32_t probe_width, u
             ac.probes = buf;
             ac.m = mc;
             ac.counts = counts ? counts + off : nullptr;
-            e = hg::probe_table(t->d, ac, s);
+            e = hg::probe_table(td, ac, s);
             if (e == cudaSuccess) e = cudaEventRecord(done[b], s);
         }
         if (ring) cudaFreeAsync(ring, s);
@@ -564,9 +604,26 @@ hg_status hg_probe_new_prepared(const hg_table* ta, const hg_table* tb,
     const bool want_pairs = opts.materialize && opts.pair_cap > 0;
     const bool pairs_dev = want_pairs && is_device_ptr(opts.pairs);
     const size_t tot_bytes = opts.device_result ? 0 : 256;
-    const size_t pr_bytes = (want_pairs && !pairs_dev) ? opts.pair_cap * 2 * opts.pair_width : 0;
-    void* scratch = nullptr;
     cudaError_t e = cudaSuccess;
+    // host pair destination: device staging sized from the exact match count
+    // (one count-only intersect first), not from pair_cap
+    uint64_t cap_eff = opts.pair_cap;
+    if (want_pairs && !pairs_dev) {
+        uint64_t* dt = nullptr;
+        uint64_t ht[2] = {0, 0};
+        e = cudaMallocAsync(reinterpret_cast<void**>(&dt), 16, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(dt, 0, 16, s);
+        hg::IntersectArgs ca;
+        ca.totals = dt;
+        if (e == cudaSuccess) e = hg::intersect_tables(ta->d, tb->d, ca, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(ht, dt, 16, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (dt) cudaFreeAsync(dt, s);
+        if (e != cudaSuccess) return cuda_fail(e, "hg_probe_new_prepared: match count");
+        cap_eff = std::max<uint64_t>(1, std::min(opts.pair_cap, ht[0]));
+    }
+    const size_t pr_bytes = (want_pairs && !pairs_dev) ? cap_eff * 2 * opts.pair_width : 0;
+    void* scratch = nullptr;
     if (tot_bytes + pr_bytes && (e = cudaMallocAsync(&scratch, tot_bytes + pr_bytes, s)) != cudaSuccess)
         return cuda_fail(e, "hg_probe_new_prepared: scratch");
     uint64_t* totals = opts.device_result ? opts.device_result : static_cast<uint64_t*>(scratch);
@@ -577,7 +634,7 @@ hg_status hg_probe_new_prepared(const hg_table* ta, const hg_table* tb,
     ia.totals = totals;
     ia.pairs = pairs;
     ia.pair_bytes = opts.pair_width;
-    ia.cap = want_pairs ? opts.pair_cap : 0;
+    ia.cap = want_pairs ? cap_eff : 0;
     if (e == cudaSuccess) e = hg::intersect_tables(ta->d, tb->d, ia, s);
     hg_status st = HG_OK;
     if (e != cudaSuccess) {
@@ -622,7 +679,6 @@ hg_status hg_probe_new(const void* keys_a, uint64_t na, const void* keys_b, uint
         if (st != HG_OK) return st;
     }
     cfg.variant = HG_BUILD_BINNED;  // join.hpp:173-174
-    if (cfg.vertex_count > (uint64_t(1) << 30)) cfg.variant = HG_BUILD_SIMPLE;  // same table
     hg_table* ta = nullptr;
     hg_table* tb = nullptr;
     hg_status st = hg_build(keys_a, key_width, nullptr, 8, na, &cfg, stream, &ta);
@@ -633,7 +689,25 @@ hg_status hg_probe_new(const void* keys_a, uint64_t na, const void* keys_b, uint
     return st;
 }
 
+static hg_status count_instances_impl(const hg_table* t, uint64_t key, const hg_probe_options* o,
+                                      uint64_t* out, void* stream);
+
 hg_status hg_count_instances(const hg_table* t, uint64_t key, uint64_t* out, void* stream) {
+    return count_instances_impl(t, key, nullptr, out, stream);
+}
+
+hg_status hg_count_instances_hasher(const hg_table* t, uint64_t key, int32_t hash_kind,
+                                    uint64_t hash_seed, uint64_t* out, void* stream) {
+    hg_probe_options o;
+    hg_probe_options_init(&o);
+    o.flags = HG_PROBE_HASHER;
+    o.hash_kind = hash_kind;
+    o.hash_seed = hash_seed;
+    return count_instances_impl(t, key, &o, out, stream);
+}
+
+static hg_status count_instances_impl(const hg_table* t, uint64_t key, const hg_probe_options* o,
+                                      uint64_t* out, void* stream) {
     if (!out) return fail(HG_EINVAL, "out is NULL");
     if (t && t->d.key_bytes == 4 && key > 0xFFFFFFFFull) {
         // A u32-keyed table cannot hold a wider key: zero matches (the
@@ -645,14 +719,24 @@ hg_status hg_count_instances(const hg_table* t, uint64_t key, uint64_t* out, voi
     const uint32_t k32 = uint32_t(key);
     const void* kp = t && t->d.key_bytes == 4 ? static_cast<const void*>(&k32)
                                                : static_cast<const void*>(&key);
-    hg_status st = hg_probe(t, kp, t ? t->d.key_bytes : 8, 1, nullptr, &r, stream);
+    hg_status st = hg_probe(t, kp, t ? t->d.key_bytes : 8, 1, o, &r, stream);
     if (st == HG_OK) *out = r.match_count;
     return st;
 }
 
 hg_status hg_validate(const hg_table* t, const void* input_keys, uint64_t expected_entries,
                       int32_t* violation, void* stream) {
+    if (!t) return fail(HG_EINVAL, "NULL argument");
+    return hg_validate_hasher(t, input_keys, expected_entries, t->d.hash_kind, t->d.seed, violation,
+                              stream);
+}
+
+hg_status hg_validate_hasher(const hg_table* t, const void* input_keys, uint64_t expected_entries,
+                             int32_t hash_kind, uint64_t hash_seed, int32_t* violation,
+                             void* stream) {
     if (!t || !violation) return fail(HG_EINVAL, "NULL argument");
+    if (hash_kind != HG_HASH_MIX64 && hash_kind != HG_HASH_IDENTITY)
+        return fail(HG_EINVAL, "unknown hash_kind");
     if (cudaSetDevice(t->device) != cudaSuccess) return fail(HG_ECUDA, "cudaSetDevice failed");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     *violation = 0;
@@ -660,14 +744,14 @@ hg_status hg_validate(const hg_table* t, const void* input_keys, uint64_t expect
         *violation = 1;
         return HG_OK;
     }
-    if (t->d.n != expected_entries) {
-        // offsets[V] vs edges is checked on device; edge count vs input size here (core.hpp:268)
-    }
     DevIn in;
     cudaError_t e = in.stage(input_keys, t->d.n * t->d.key_bytes, s);
     uint32_t* d_code = nullptr;
     if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&d_code), 4, s);
-    if (e == cudaSuccess) e = hg::validate_table(t->d, input_keys ? in.ptr : nullptr, d_code, s);
+    hg::TableDesc td = t->d;  // core.hpp:271: the check uses the caller's hasher
+    td.hash_kind = hash_kind;
+    td.seed = hash_seed;
+    if (e == cudaSuccess) e = hg::validate_table(td, input_keys ? in.ptr : nullptr, d_code, s);
     uint32_t code = 0;
     if (e == cudaSuccess) e = cudaMemcpyAsync(&code, d_code, 4, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -717,7 +801,8 @@ hg_status hg_route(const void* keys, int32_t key_width, const void* vals, int32_
     uint64_t* dc = shard_counts;
     if (!counts_dev) HG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dc), shards * 8, s));
     cudaError_t e = hg::route_keys(keys, key_width, vals, val_width, n, val_base, hash_seed,
-                                   hash_kind, global_vertices, shards, out_keys, out_vals, dc, s);
+                                   hash_kind, global_vertices, 0, global_vertices, 0, shards,
+                                   out_keys, out_vals, dc, s);
     if (e == cudaSuccess && !counts_dev) {
         e = cudaMemcpyAsync(shard_counts, dc, shards * 8, cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);

@@ -16,6 +16,8 @@ struct TableDesc {
     uint64_t n = 0;         // N
     uint64_t gnv = 0;       // global vertex count of a hash-range shard (0 = nv)
     uint64_t vbase = 0;     // first global vertex owned by this shard
+    uint64_t obase = 0;     // entry base added to every offset written (a vertex-range
+                            // slice of a larger table, build_v2_sliced)
     uint64_t seed = 0;
     int hash_kind = 0;      // 0 mix64, 1 identity
     int key_bytes = 4;      // 4 | 8
@@ -84,17 +86,22 @@ cudaError_t validate_table(const TableDesc& t, const void* input_keys, uint32_t*
                            cudaStream_t s);
 
 int num_sms();
+size_t smem_optin();  // opt-in shared memory per CTA (227 KB on B200)
 
 // Vertex-space divisor of a table: global V (sharded) or V, with the shard base.
 inline uint64_t global_nv(const TableDesc& t) { return t.gnv ? t.gnv : t.nv; }
 
 // Hash-range routing: groups n keys (+ values, or
-// implicit values val_base + i) by owner shard = (h(key) mod V) / ceil(V/G)
-// into SoA out_keys/out_vals; shard_counts[G] (device, u64) receives the
-// number of keys per shard. G <= 256.
+// implicit values val_base + i) by owner shard = ((h(key) mod V) - vertex_base)
+// / span (span 0: ceil(local_vertices / G)) into SoA out_keys/out_vals;
+// shard_counts[G] (device, u64) receives the number of keys per shard.
+// G <= 256. Multi-GPU routing uses vertex_base = 0, local_vertices = V, span 0;
+// the sliced binned build routes a table's own vertex range
+// [vertex_base, vertex_base + local_vertices) into power-of-two spans.
 cudaError_t route_keys(const void* keys, int key_bytes, const void* vals, int val_bytes,
                        uint64_t n, uint64_t val_base, uint64_t seed, int hash_kind,
-                       uint64_t global_vertices, uint32_t shards, void* out_keys, void* out_vals,
+                       uint64_t global_vertices, uint64_t vertex_base, uint64_t local_vertices,
+                       uint64_t span, uint32_t shards, void* out_keys, void* out_vals,
                        uint64_t* shard_counts, cudaStream_t s);
 
 // Kernel timeline hooks (hg_prof.cu).

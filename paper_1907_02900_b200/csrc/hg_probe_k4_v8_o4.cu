@@ -1,0 +1,6 @@
+// Instantiates probe_pow for 4-byte keys, 8-byte values, 4-byte offsets.
+#include "hg_probe_impl.cuh"
+
+namespace hg {
+template cudaError_t probe_pow<uint32_t, uint64_t, uint32_t>(const TableDesc&, const ProbeArgs&, cudaStream_t);
+}  // namespace hg

@@ -1,0 +1,6 @@
+// Instantiates probe_pow for 8-byte keys, 8-byte values, 8-byte offsets.
+#include "hg_probe_impl.cuh"
+
+namespace hg {
+template cudaError_t probe_pow<uint64_t, uint64_t, uint64_t>(const TableDesc&, const ProbeArgs&, cudaStream_t);
+}  // namespace hg

@@ -70,9 +70,11 @@ __device__ __forceinline__ uint64_t hv(uint64_t key, uint64_t seed, int hk, cons
 
 // ------------------------------------------------------------ geometry
 
+constexpr uint32_t kMaxPartShift = 15;
+
 struct PartGeom {
     uint32_t pshift = 0;  // partition width P = 2^pshift vertices
-    uint64_t nparts = 1;  // ceil(V / P) <= 2^16
+    uint64_t nparts = 1;  // ceil(V / P)
     uint32_t bits = 0;    // ceil(log2(nparts))
     uint32_t b1 = 0, b2 = 0;  // digit widths (pass 1 high, pass 2 low), b1 + b2 = bits
 };
@@ -83,8 +85,11 @@ inline uint32_t ceil_log2(uint64_t x) {
     return b;
 }
 
-// Partition width: aim for ~target entries per partition (N/V * P), never
-// more than 2^16 partitions (two 8-bit digits), never wider than 2^16.
+// Partition width: aim for ~target entries per partition (N/V * P), at most
+// 2^16 partitions (two 8-bit digits) while P <= 2^15, never wider than 2^15
+// (2^15 u32 counters + K7's staging fit one CTA's 227 KB for every entry
+// type). Callers check g.bits <= 16 (2^31 < V: the binned build slices the
+// vertex range first, see build_v2_sliced).
 inline PartGeom make_geom(uint64_t nv, uint64_t n, uint64_t want_pv, double target) {
     PartGeom g;
     const uint32_t vbits = ceil_log2(nv);
@@ -94,10 +99,10 @@ inline PartGeom make_geom(uint64_t nv, uint64_t n, uint64_t want_pv, double targ
     } else {
         const double per_vertex = n ? double(n) / double(nv) : 1.0;
         ps = 0;
-        while (ps < 16 && per_vertex * double(uint64_t(2) << ps) <= target) ++ps;
+        while (ps < kMaxPartShift && per_vertex * double(uint64_t(2) << ps) <= target) ++ps;
     }
     if (vbits > 16 && ps < vbits - 16) ps = vbits - 16;
-    if (ps > 16) ps = 16;
+    if (ps > kMaxPartShift) ps = kMaxPartShift;
     if (ps > vbits) ps = vbits;
     g.pshift = ps;
     g.nparts = (nv + (uint64_t(1) << ps) - 1) >> ps;
@@ -422,22 +427,10 @@ struct PartitionScratch {
 // out[part_start[p] .. part_start[p+1]) holds the entries of partition p
 // (p = h(key) >> pshift). part_start (nparts + 1 entries, device) receives
 // the partition offsets; part_start[nparts] = n.
-// State handed to a fused consumer when partition() stops after pass 1
-// (hg_binned.cu's k_split_build runs pass 2 and the per-partition build in
-// one kernel): the pass-1 output, the pass-2 cursors and the tile layout.
-template <typename K, typename VT, typename OffT>
-struct Pass2State {
-    const typename EntryT<K, VT>::T* mid = nullptr;
-    OffT* cur2 = nullptr;
-    const uint64_t* tile_prefix = nullptr;
-    uint32_t nb1 = 0;
-};
-
 template <typename K, typename VT, typename OffT, int POW2>
 cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, int hk,
                       const Divisor& nv, const PartGeom& g, OffT* part_start, void* scratch,
-                      typename EntryT<K, VT>::T* out, cudaStream_t s, const char* const names[3],
-                      Pass2State<K, VT, OffT>* stop_after_pass1 = nullptr) {
+                      typename EntryT<K, VT>::T* out, cudaStream_t s, const char* const names[3]) {
     using PS = PartitionScratch<K, VT, OffT>;
     using E = typename EntryT<K, VT>::T;
     char* p = static_cast<char*>(scratch);
@@ -509,13 +502,6 @@ cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, 
                   part_start, 0, nullptr, tiles1, g.nparts, mid)));
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     k_tile_prefix<OffT><<<1, 32, 0, s>>>(part_start, g.nparts, nb1, g.b2, kSplitTile, tile_prefix);
-    if (stop_after_pass1) {
-        stop_after_pass1->mid = mid;
-        stop_after_pass1->cur2 = cur2;
-        stop_after_pass1->tile_prefix = tile_prefix;
-        stop_after_pass1->nb1 = nb1;
-        return cudaGetLastError();
-    }
     const uint64_t tiles2 = tiles1 + nb1;  // upper bound; exact count = tile_prefix[nb1]
     HG_LAUNCH(names[2], s,
               (ks2<<<g2, kSplitBlock, sm2, s>>>(

@@ -109,10 +109,11 @@ k_route_scatter(const K* __restrict__ keys, const VT* __restrict__ vals, uint64_
 
 template <typename K, typename VT, int POW2>
 static cudaError_t route_typed(const void* keys, const void* vals, uint64_t n, uint64_t val_base,
-                               uint64_t seed, int hk, uint64_t V, uint32_t G, void* out_keys,
-                               void* out_vals, uint64_t* shard_counts, cudaStream_t s) {
-    const Divisor gv = make_divisor(V);
-    const Divisor span = make_divisor((V + G - 1) / G);
+                               uint64_t seed, int hk, uint64_t V, uint64_t vbase, uint64_t nloc,
+                               uint64_t span_v, uint32_t G, void* out_keys, void* out_vals,
+                               uint64_t* shard_counts, cudaStream_t s) {
+    const Divisor gv = make_divisor(V, vbase);  // (h mod V) - vbase
+    const Divisor span = make_divisor(span_v ? span_v : (nloc + G - 1) / G);
     auto* counts = reinterpret_cast<unsigned long long*>(shard_counts);
     cudaError_t e = cudaMemsetAsync(counts, 0, G * 8, s);
     if (e != cudaSuccess || n == 0) return e;
@@ -146,13 +147,15 @@ static cudaError_t route_typed(const void* keys, const void* vals, uint64_t n, u
 
 cudaError_t route_keys(const void* keys, int key_bytes, const void* vals, int val_bytes,
                        uint64_t n, uint64_t val_base, uint64_t seed, int hash_kind,
-                       uint64_t global_vertices, uint32_t shards, void* out_keys, void* out_vals,
+                       uint64_t global_vertices, uint64_t vertex_base, uint64_t local_vertices,
+                       uint64_t span, uint32_t shards, void* out_keys, void* out_vals,
                        uint64_t* shard_counts, cudaStream_t s) {
     const int hm = hash_mode(global_vertices, hash_kind);
 #define HG_ROUTE(K, VT)                                                                        \
     return dispatch_hash_mode(hm, [&](auto m) {                                                \
         return route_typed<K, VT, decltype(m)::value>(keys, vals, n, val_base, seed, hash_kind, \
-                                                      global_vertices, shards, out_keys,       \
+                                                      global_vertices, vertex_base,            \
+                                                      local_vertices, span, shards, out_keys,  \
                                                       out_vals, shard_counts, s);              \
     })
     if (key_bytes == 4) {

@@ -368,10 +368,12 @@ def build_v2(keys, cfg: Optional[BuildConfig] = None, stats: Optional[BuildStats
 
 
 def probe_standard(hg: HashGraph, probe_keys, opts: Optional[ProbeOptions] = None,
-                   counts=None, method: int = 0) -> JoinResult:
+                   counts=None, method: int = 0, host_ready: bool = False) -> JoinResult:
     """join.hpp:110-136. `counts` (optional, length-m uint32 array / CUDA
     tensor) receives each probe's match count. method: 0 auto, 1 direct
-    gathers, 2 vertex-range partitioned probes."""
+    gathers, 2 vertex-range partitioned probes. host_ready: pinned host probes
+    already hold their final contents, so their host->device copies may
+    overlap earlier work on the stream (HG_PROBE_HOST_READY)."""
     opts = opts or ProbeOptions()
     pa = _Arr(probe_keys, np.uint64 if hg.key_width == 8 else np.uint32)
     if pa.width == 8 and hg.key_width == 4:
@@ -386,9 +388,10 @@ def probe_standard(hg: HashGraph, probe_keys, opts: Optional[ProbeOptions] = Non
     o.pair_width = 8
     o.pair_cap = int(opts.pair_cap)
     o.method = int(method)
+    o.flags = 1 if host_ready else 0
     pairs = None
     if opts.materialize:
-        pairs = np.zeros(max(min(int(opts.pair_cap), max(pa.n, 1) * max(hg.num_edges(), 1)), 0),
+        pairs = np.empty(max(min(int(opts.pair_cap), max(pa.n, 1) * max(hg.num_edges(), 1)), 0),
                          MATCH_PAIR_DTYPE)
         o.pairs = pairs.ctypes.data if pairs.size else None
         if pairs.size == 0:

@@ -25,3 +25,22 @@ def test_dropin_suite_on_gpu(cuda):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+REF_BIN = os.path.join(ROOT, "tests", "cpp", "ref_tests")
+
+
+@pytest.mark.gpu
+def test_reference_unit_tests_unmodified_on_gpu(cuda):
+    """The reference's own Catch2 suites (proj/tests/test_core.cpp,
+    test_join.cpp, test_hash.cpp), compiled UNMODIFIED against
+    include/hashgraph/ through the Catch2 shim (Makefile: tests/cpp/ref_tests,
+    built where /root/reference exists; the binary travels to the GPU box),
+    every build / probe / validate running on the device through libhg_b200.so."""
+    if not os.path.exists(REF_BIN):
+        pytest.skip("tests/cpp/ref_tests not built (needs /root/reference at build time)")
+    r = subprocess.run([REF_BIN], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert " 0 failed" in r.stdout
+    assert r.stdout.count("PASS ") >= 39

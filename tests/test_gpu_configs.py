@@ -189,24 +189,6 @@ def test_pipelined_host_probes(cuda):
     assert (r2.match_count, r2.key_comparisons) == (r.match_count, r.key_comparisons)
 
 
-def test_fused_split_build_opt_in(oracle, cuda, monkeypatch):
-    """HG_FUSE=1 selects the fused pass-2 + partition-build kernel (K67); its
-    tables must equal the oracle's like the default path's."""
-    monkeypatch.setenv("HG_FUSE", "1")
-    n = 1 << 22
-    keys = cuda.empty(n, dtype=cuda.int32, device="cuda")
-    hg.generate(keys, kind=0, seed=9)
-    host = keys.cpu().numpy().view(np.uint32).astype(np.uint64)
-    for load in (1.0, 0.5, 2.0):
-        t = hg.build_v2(keys, BuildConfig(load_factor=load))
-        canon_equal(t, oracle.build(host, variant=2, load=load))
-    # heavy keys: oversized partitions through the K7b path
-    keys[: n // 8] = 12345
-    host = keys.cpu().numpy().view(np.uint32).astype(np.uint64)
-    t = hg.build_v2(keys)
-    canon_equal(t, oracle.build(host, variant=2))
-
-
 def test_key_files_device(tmp_path, cuda):
     """HGKEYS01 straight to / from device memory (pinned staging chunks), then
     a build from the loaded keys equals the build from the originals."""
