@@ -43,8 +43,57 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-extras", action="store_true", help="skip the per-phase/variant breakdown")
-    p.add_argument("--cpu-log2n", type=int, default=22)
+    p.add_argument("--cpu-log2n", type=int, default=None,
+                   help="reference-arm sample size (default: the B200 arm's own --log2n, "
+                        "i.e. the same config)")
+    p.add_argument("--csv", default="bench_rows.csv",
+                   help="reference bench CSV rows (hashgraph_bench.cpp:47-49 + B200 columns)")
     return p.parse_args()
+
+
+def workload_config(log2n: int, variant: int, world: int) -> dict:
+    """The `config` of both arms' JSON lines (identical for the same args)."""
+    n = 1 << log2n
+    return {"workload": f"C2: build_v{variant} over 2^{log2n} uniform u32 keys (splitmix64 "
+                        f"seed 1) at load 1 + probe_standard (count) of 2^{log2n} u32 probes "
+                        f"(seed 2), per GPU",
+            "n_per_gpu": n, "m_per_gpu": n, "load_factor": 1.0, "variant": variant,
+            "vertices": n,
+            "l2": "inputs larger than L2 (1 GiB keys + 1 GiB probes per GPU vs 126 MB L2)",
+            "parallelism": f"hash-range shards x{world}" if world > 1 else "1 GPU"}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# SURVEY.md 8(d) reference-loop-nest bytes (the roofline numerators of the
+# phase figures): sk/sv/so key/value/offset widths, sc = 4-byte counters.
+def ref_bytes_build(variant, n, v, sk=4, sv=4, so=4, sc=4, bins=1 << 15):
+    if variant == 1:
+        return n * (3 * sk + sv) + v * (7 * sc + 2 * so) + so
+    b = min(bins, v)
+    return n * (6 * sk + 3 * sv) + (v + b) * (7 * sc + 2 * so) + 2 * so
+
+
+def ref_bytes_probe(m, v, c, sk=4, so=4, sc=4):
+    return m * sk + (v + 1) * so + c * sk + m * sc
+
+
+def ref_bytes_probe_pairs(m, v, c, p, sk=4, so=4, sc=4, sv=4, si=4):
+    return (ref_bytes_probe(m, v, c, sk, so, sc) + m * sc + (m + 1) * 8 +
+            m * sk + (v + 1) * so + c * sk + 8 * m + p * sv + 2 * p * si)
+
+
+def roof(bytes_, ms, peak):
+    gbs = bytes_ / (ms * 1e-3) / 1e9
+    return {"alg_bytes": int(bytes_), "achieved_gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}
 
 
 # ------------------------------------------------------------------ helpers
@@ -155,17 +204,21 @@ def reference_alg_bytes(variant: int, n: int, v: int, m: int, c: int, kb: int = 
 
 # ------------------------------------------------------------------ reference arm
 
-def cpu_reference_rate(variant: int, log2n: int, trials: int, warmup: int):
+def cpu_reference_rate(variant: int, log2n: int, trials: int, warmup: int, threads=None):
     """The reference's own CPU implementation (oracle/_ref = the unmodified
-    reference headers; oracle port when _ref is absent) on the host cores:
-    build + probe_standard of a 2^log2n sample of the same workload."""
+    reference headers, -O3 x86-64-v4 on AVX-512 hosts; oracle port when _ref
+    is absent) on the host cores: build + probe_standard of 2^log2n keys and
+    probes of the same workload (table allocation inside the timed region, as
+    in the reference bench)."""
     from oracle.oracle import Oracle, Reference, have_reference
     n = 1 << log2n
     keys = splitmix_u32(1, 0, n).astype(np.uint64)
     probes = splitmix_u32(2, 0, n).astype(np.uint64)
-    threads = os.cpu_count() or 1
+    threads = threads or os.cpu_count() or 1
+    so = None
     if have_reference():
         ref, kind = Reference(), "reference"
+        so = os.path.basename(ref.path)
         ref.set_threads(threads)
 
         def one():
@@ -191,25 +244,34 @@ def cpu_reference_rate(variant: int, log2n: int, trials: int, warmup: int):
             "sample": f"build_v{variant} + probe_standard (count) of 2^{log2n} u32 keys "
                       f"(splitmix seed 1) and 2^{log2n} probes (seed 2), load 1; median of "
                       f"{trials} after {warmup} warm-up; HASHGRAPH_THREADS={threads}",
-            "seconds_median": med, "seconds": times}
+            "seconds_median": med, "seconds": times, "cpu_model": cpu_model(),
+            "nproc": os.cpu_count(), "library": so}
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU implementation on the box's
+    host cores, all threads, on this arm's config (2^log2n keys + probes per
+    step; at N > 1 rank 0 runs one GPU's share as the sample)."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
+    log2n = args.cpu_log2n or args.log2n
     steps = max(1, args.steps)
-    res = cpu_reference_rate(args.variant, args.cpu_log2n, steps, args.warmup)
-    n = 1 << args.cpu_log2n
+    # each step is a full 2^28 build + probe (~10-20 s on 16 cores): cap the
+    # warm-up so K steps + W warm-ups end within a few minutes
+    warm = min(args.warmup, 1)
+    res = cpu_reference_rate(args.variant, log2n, steps, warm)
+    cfg = workload_config(args.log2n, args.variant, world)
     line = {
         "impl": "reference", "metric": METRIC, "value": res["value"], "unit": "Gkeys/s",
-        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+        "n_gpus": args.gpus, "steps": steps, "warmup": warm,
         "ms_per_step": res["seconds_median"] * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": f"C2 sample on host cores: build_v{args.variant} + "
-                               f"probe_standard, 2^{args.cpu_log2n} u32 keys + probes, load 1",
-                   "n": n, "m": n, "load_factor": 1.0, "variant": args.variant},
-        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "config": cfg,
+        "same_config": log2n == args.log2n and world == 1,
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                              "cpu_model", "nproc", "library")},
         "e2e": {"value": res["value"], "unit": "Gkeys/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -231,31 +293,55 @@ def _timed(torch, stream, fn, reps=3):
     return e0.elapsed_time(e1) / reps
 
 
-def bench_c3(torch, hg, stream, sp, log2n=28):
+def bench_c3(torch, hg, stream, sp, peak, rows, log2n=28):
     """C3: 2^28 u64 keys ~ Zipf(s = 1.0) over 2^24 ranks with u64 values,
-    binned and simple builds across the load sweep (G keys/s = N / t)."""
+    binned and simple builds across the load sweep (G keys/s = N / t), and
+    probe_standard (count) of 2^28 probes drawn from the same Zipf
+    distribution (seed 2: heavy ranks hit long segments) into each V2 table
+    (G probes/s = M / t). Rooflines from SURVEY.md 8(d) bytes with the exact C."""
     n = 1 << log2n
     cdf = torch.tensor(hg.zipf_cdf(1 << 24, 1.0), dtype=torch.float64, device="cuda")
     keys = torch.empty(n, dtype=torch.int64, device="cuda")
     hg.generate(keys, kind=3, seed=1, ref=cdf)
+    probes = torch.empty(n, dtype=torch.int64, device="cuda")
+    hg.generate(probes, kind=3, seed=2, ref=cdf)
     vals = torch.arange(n, dtype=torch.int64, device="cuda")
-    out = {"workload": "2^28 u64 Zipf(1.0) keys over 2^24 ranks, u64 values = position"}
+    res = torch.zeros(2, dtype=torch.int64, device="cuda")
+    out = {"workload": "2^28 u64 Zipf(1.0) keys over 2^24 ranks, u64 values = position; "
+                       "2^28 Zipf(1.0) probes (seed 2)"}
     for load in (0.5, 1.0, 1.5, 2.0, 4.0):
         row = {}
-        for name, bfn in (("v2", hg.build_v2), ("v1", hg.build_v1)):
+        nv = hg.derived_vertex_count(n, load)
+        so = 4 if nv <= (1 << 32) else 8
+        for name, var, bfn in (("v2", 2, hg.build_v2), ("v1", 1, hg.build_v1)):
             cfg = hg.BuildConfig(load_factor=load)
             ms = _timed(torch, stream, lambda: bfn(keys, cfg, vals=vals, stream=sp).close(sp),
                         reps=2 if name == "v1" else 3)
-            row[name] = {"build_ms": round(ms, 3), "build_gkeys_s": round(n / (ms * 1e-3) / 1e9, 3)}
+            row[name] = {"build_ms": round(ms, 3), "build_gkeys_s": round(n / (ms * 1e-3) / 1e9, 3),
+                         "roofline": roof(ref_bytes_build(var, n, nv, 8, 8, so), ms, peak)}
+            rows.append(csv_row("build", f"hg_{name}", n, load, ms, n, mult="zipf1.0",
+                                alg=row[name]["roofline"]))
+        t = hg.build_v2(keys, hg.BuildConfig(load_factor=load), vals=vals, stream=sp)
+        ms = _timed(torch, stream, lambda: hg.probe_device(t, probes, res, stream=sp))
+        res.zero_()
+        hg.probe_device(t, probes, res, stream=sp)
+        mc, cmp = (int(x) for x in res.cpu().tolist())
+        t.close(sp)
+        row["probe"] = {"probe_ms": round(ms, 3), "gprobes_s": round(n / (ms * 1e-3) / 1e9, 3),
+                        "match_count": mc, "key_comparisons": cmp,
+                        "roofline": roof(ref_bytes_probe(n, nv, cmp, 8, so), ms, peak)}
+        rows.append(csv_row("probe", "probe_standard", n, load, ms, n, mult="zipf1.0", matches=mc,
+                            alg=row["probe"]["roofline"]))
         out[f"load_{load}"] = row
-    del keys, vals
+    del keys, vals, probes
     torch.cuda.empty_cache()
     return out
 
 
-def bench_c4(torch, hg, stream, sp):
+def bench_c4(torch, hg, stream, sp, peak, rows):
     """C4: probe_standard with pairs, 2^29 probes into 2^28 unique u32 build
-    keys at hit ratio 0.1 / 0.5 / 1.0 (G probes/s = M / t, u32 pairs)."""
+    keys at hit ratio 0.1 / 0.5 / 1.0 (G probes/s = M / t, u32 pairs);
+    roofline from SURVEY.md 8(d)'s pairs formula with the exact C and P."""
     n, m = 1 << 28, 1 << 29
     build = torch.empty(n, dtype=torch.int32, device="cuda")
     hg.generate(build, kind=2)
@@ -268,14 +354,71 @@ def bench_c4(torch, hg, stream, sp):
         hg.generate(probes, kind=1, seed=3, hit=h, ref=build)
         ms = _timed(torch, stream, lambda: hg.probe_device(t, probes, res, pairs=pairs,
                                                            pair_width=4, pair_cap=m, stream=sp))
+        res.zero_()
+        hg.probe_device(t, probes, res, pairs=pairs, pair_width=4, pair_cap=m, stream=sp)
         mc, cmp = (int(x) for x in res.cpu().tolist())
         out[f"hit_{h}"] = {"probe_ms": round(ms, 3),
                            "gprobes_s": round(m / (ms * 1e-3) / 1e9, 3),
-                           "match_count": mc, "key_comparisons": cmp}
+                           "match_count": mc, "key_comparisons": cmp,
+                           "roofline": roof(ref_bytes_probe_pairs(m, n, cmp, mc), ms, peak)}
+        rows.append(csv_row("probe", "probe_standard", m, 1.0, ms, m, mult=f"hit{h}", matches=mc,
+                            alg=out[f"hit_{h}"]["roofline"]))
     t.close(sp)
     del build, probes, pairs
     torch.cuda.empty_cache()
     return out
+
+
+def bench_multiplicity(torch, hg, stream, sp, peak, rows, log2n=28):
+    """build_v2 at key multiplicity 1 vs 32 (acceptance_main.cpp:234-273,
+    criterion 4; the paper reports < 15 % slowdown). Keys come
+    from the reference's own generator (keygen.hpp:59-73, uniform_multiplicity,
+    sequential mt19937_64 -- oracle/_ref) handed over as HGKEYS01 files and
+    read straight into device memory (hg_keys_read)."""
+    import tempfile
+    from oracle.oracle import Reference, have_reference
+    if not have_reference():
+        return {"skipped": "oracle/_ref (compiled reference generator) absent"}
+    n = 1 << log2n
+    ref = Reference()
+    out = {"workload": f"build_v2 of 2^{log2n} keys from keygen uniform_multiplicity "
+                       f"(seeds 101 / 102, hash_seed 9 as acceptance criterion 4), u32 on device"}
+    rates = {}
+    keys = torch.empty(n, dtype=torch.int32, device="cuda")
+    with tempfile.TemporaryDirectory() as d:
+        for mult, seed in ((1.0, 101), (32.0, 102)):
+            path = os.path.join(d, f"m{int(mult)}.keys")
+            ref.write_keys(path, ref.generate(1, n, mult, seed))
+            hg.read_keys(path, out=keys)
+            os.unlink(path)
+            cfg = hg.BuildConfig(hash_seed=9)
+            ms = _timed(torch, stream, lambda: hg.build_v2(keys, cfg, stream=sp).close(sp))
+            rates[mult] = n / (ms * 1e-3) / 1e9
+            out[f"mult_{int(mult)}"] = {"build_ms": round(ms, 3),
+                                       "build_gkeys_s": round(rates[mult], 3),
+                                       "roofline": roof(ref_bytes_build(2, n, n), ms, peak)}
+            rows.append(csv_row("build", "hg_v2", n, 1.0, ms, n, mult=str(mult), seed=seed,
+                                alg=out[f"mult_{int(mult)}"]["roofline"]))
+    out["slowdown_32_vs_1"] = round(1.0 - rates[32.0] / rates[1.0], 4)
+    del keys
+    torch.cuda.empty_cache()
+    return out
+
+
+CSV_HEADER = ("experiment,algo,n,load_factor,bins,multiplicity,seed,trials,threads,"
+              "median_seconds,keys_per_second,match_count,truncated,"
+              "gpus,bytes_algorithmic,roofline_achieved,dram_bytes_measured,cpu_cores")
+
+
+def csv_row(experiment, algo, n, load, ms, keys, mult="1", seed=1, matches=0, alg=None,
+            trials=3, gpus=1, threads=0, dram=""):
+    """One row of the reference bench's CSV (hashgraph_bench.cpp:47-49,
+    CsvWriter::row) extended per SURVEY.md 5 with gpus, bytes_algorithmic,
+    roofline_achieved, dram_bytes_measured and cpu_cores."""
+    sec = ms * 1e-3
+    return (f"{experiment},{algo},{n},{load:g},{1 << 15},{mult},{seed},{trials},{threads},"
+            f"{sec:.9f},{keys / sec:.3f},{matches},0,{gpus},"
+            f"{alg['alg_bytes'] if alg else ''},{alg['frac'] if alg else ''},{dram},{threads}")
 
 
 # ------------------------------------------------------------------ B200 arm
@@ -376,6 +519,7 @@ def run_b200(args):
                                       for k in kern) // max(1, args.steps)}
     ref_bytes = reference_alg_bytes(args.variant, local_n, local_v, local_m,
                                     comparisons if world == 1 else int(engine.last_local_c))
+    roofline["step_alg_frac"] = round(roofline["step_alg_bytes"] / (ms * 1e-3) / 1e9 / peak, 4)
     roofline["step_reference_alg_bytes"] = ref_bytes
     roofline["step_reference_frac"] = round(ref_bytes / (ms * 1e-3) / 1e9 / peak, 4)
     kernels = {k: {"launches": l, "avg_ms": round(t / l, 4), "share": round(t / sum(
@@ -386,13 +530,7 @@ def run_b200(args):
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic",
-        "config": {"workload": f"C2: build_v{args.variant} over 2^{args.log2n} uniform u32 keys "
-                               f"(splitmix64 seed 1) at load 1 + probe_standard (count) of "
-                               f"2^{args.log2n} u32 probes (seed 2), per GPU",
-                   "n_per_gpu": n, "m_per_gpu": m, "load_factor": 1.0, "variant": args.variant,
-                   "vertices": nv * (1 if world == 1 else 1),
-                   "l2": "inputs larger than L2 (1 GiB keys + 1 GiB probes per GPU vs 126 MB L2)",
-                   "parallelism": f"hash-range shards x{world}" if world > 1 else "1 GPU"},
+        "config": workload_config(args.log2n, args.variant, world),
         "roofline": roofline,
         "clocks": clocks.summary(),
         "gpu_launches": gpu_launches,
@@ -401,6 +539,11 @@ def run_b200(args):
     }
 
     # ---- per-phase / per-variant breakdown (device-resident, outside the timed region)
+    rows = []
+    rows.append(csv_row("join", f"hg_v{args.variant}+probe_standard", n, 1.0, ms, n + m,
+                        matches=matches, trials=args.steps, gpus=world,
+                        alg={"alg_bytes": roofline["step_alg_bytes"],
+                             "frac": roofline["step_alg_frac"]}))
     if not args.no_extras and world == 1:
         extras = {}
         for var, bfn in ((1, hg.build_v1), (2, hg.build_v2)):
@@ -417,10 +560,18 @@ def run_b200(args):
                 torch.cuda.synchronize()
                 tb += e0.elapsed_time(e1)
                 tp += e1.elapsed_time(e2)
-            extras[f"v{var}"] = {"build_ms": round(tb / reps, 4),
-                                 "build_gkeys_s": round(n / (tb / reps * 1e-3) / 1e9, 3),
-                                 "probe_ms": round(tp / reps, 4),
-                                 "probe_gkeys_s": round(m / (tp / reps * 1e-3) / 1e9, 3)}
+            bms, pms = tb / reps, tp / reps
+            extras[f"v{var}"] = {"build_ms": round(bms, 4),
+                                 "build_gkeys_s": round(n / (bms * 1e-3) / 1e9, 3),
+                                 "build_roofline": roof(ref_bytes_build(var, n, nv), bms, peak),
+                                 "probe_ms": round(pms, 4),
+                                 "probe_gkeys_s": round(m / (pms * 1e-3) / 1e9, 3),
+                                 "probe_roofline": roof(ref_bytes_probe(m, nv, comparisons), pms,
+                                                        peak)}
+            rows.append(csv_row("build", f"hg_v{var}", n, 1.0, bms, n,
+                                alg=extras[f"v{var}"]["build_roofline"]))
+            rows.append(csv_row("probe", "probe_standard", m, 1.0, pms, m, matches=matches,
+                                alg=extras[f"v{var}"]["probe_roofline"]))
         # probe_new (join.hpp:170-182): second table over the probes with the
         # shared V, then the K12 intersect (count only)
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
@@ -448,12 +599,16 @@ def run_b200(args):
             "build_b_ms": round(tb / reps, 4), "intersect_ms": round(ti / reps, 4),
             "intersect_gkeys_s": round((n + m) / (ti / reps * 1e-3) / 1e9, 3),
             "intersect_alg_gbs": round(ib / (ti / reps * 1e-3) / 1e9, 1),
+            "intersect_roofline": roof(ib, ti / reps, peak),
             "join_gkeys_s": round((n + m) / ((tb / reps + extras["v2"]["build_ms"] + ti / reps)
                                              * 1e-3) / 1e9, 3),
             "match_count": pn_matches, "key_comparisons": pn_cmp,
             "matches_equal_probe_standard": pn_matches == matches}
-        extras["c3_zipf"] = bench_c3(torch, hg, stream, sp)
-        extras["c4_join"] = bench_c4(torch, hg, stream, sp)
+        rows.append(csv_row("probe", "probe_new", n + m, 1.0, ti / reps, n + m,
+                            matches=pn_matches, alg=extras["probe_new"]["intersect_roofline"]))
+        extras["c3_zipf"] = bench_c3(torch, hg, stream, sp, peak, rows)
+        extras["c4_join"] = bench_c4(torch, hg, stream, sp, peak, rows)
+        extras["multiplicity"] = bench_multiplicity(torch, hg, stream, sp, peak, rows)
         line["phases"] = extras
 
     # ---- e2e through the public API with pinned HOST buffers
@@ -464,7 +619,9 @@ def run_b200(args):
 
         def e2e_step():
             t = build(hkeys, stream=sp)           # H2D of the keys inside hg_build
-            r = hg.probe_standard(t, hprobes)     # H2D of probes, D2H of the totals, sync
+            # H2D of the probes (chunked, overlapping the build still running:
+            # the pinned buffer is final, HG_PROBE_HOST_READY), D2H of the totals
+            r = hg.probe_standard(t, hprobes, host_ready=True)
             t.close(sp)
             return r
 
@@ -518,11 +675,24 @@ def run_b200(args):
                                "hg_route / hg_build / hg_probe, NCCL all_to_all) -> totals"}
 
     if not args.no_cpu and world == 1 and rank == 0:
+        # the reference on the host cores: the same 2^28 config, all threads,
+        # two trials (~30 s of CPU work), plus a 1-thread row on a 2^22 sample
         try:
-            cb = cpu_reference_rate(args.variant, args.cpu_log2n, trials=5, warmup=1)
-            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            keys_ = ("value", "unit", "cores", "kind", "sample", "cpu_model", "nproc", "library")
+            cb = cpu_reference_rate(args.variant, args.cpu_log2n or args.log2n, trials=2, warmup=0)
+            line["cpu_baseline"] = {k: cb[k] for k in keys_}
+            c1 = cpu_reference_rate(args.variant, 22, trials=3, warmup=1, threads=1)
+            line["cpu_baseline"]["threads_1"] = {k: c1[k] for k in ("value", "unit", "cores",
+                                                                     "sample")}
+            rows.append(csv_row("join", f"ref_hg_v{args.variant}+probe_standard", n, 1.0,
+                                cb["seconds_median"] * 1e3, 2 * (1 << (args.cpu_log2n or args.log2n)),
+                                trials=2, gpus=0, threads=cb["cores"]))
         except Exception as ex:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "error": str(ex)}
+    if rank == 0 and args.csv:
+        with open(args.csv, "w") as f:
+            f.write(CSV_HEADER + "\n" + "\n".join(rows) + "\n")
+        line["csv"] = args.csv
 
     if rank == 0:
         print(json.dumps(line), flush=True)

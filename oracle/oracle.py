@@ -22,6 +22,22 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "libhgoracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libhgref.so")
+REF_SO_V4 = os.path.join(HERE, "_ref", "libhgref_v4.so")
+
+
+def cpu_has_avx512() -> bool:
+    """x86-64-v4 feature set (avx512 f/bw/cd/dq/vl) on this host."""
+    try:
+        flags = next(l for l in open("/proc/cpuinfo") if l.startswith("flags")).split()
+    except (OSError, StopIteration):
+        return False
+    return all(f in flags for f in ("avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl"))
+
+
+def reference_so() -> str:
+    """The compiled reference to time: the x86-64-v4 build on AVX-512 hosts,
+    else the portable x86-64-v2 build."""
+    return REF_SO_V4 if os.path.exists(REF_SO_V4) and cpu_has_avx512() else REF_SO
 
 HASH_MIX64 = 0
 HASH_IDENTITY = 1
@@ -260,11 +276,13 @@ class Reference:
     """The reference headers themselves (oracle/_ref). Threads follow
     HASHGRAPH_THREADS (parallel.hpp:25-34); ``threads`` sets it per call."""
 
-    def __init__(self, path: str = REF_SO):
+    def __init__(self, path: str | None = None):
+        path = path or reference_so()
         if not os.path.exists(path):
             build_oracle()
         if not os.path.exists(path):
             raise FileNotFoundError(f"{path} (reference not compiled here)")
+        self.path = path
         lib = C.CDLL(path)
         u64, dbl, i32, vp = C.c_uint64, C.c_double, C.c_int, C.c_void_p
         lib.hgr_mix64.restype = u64

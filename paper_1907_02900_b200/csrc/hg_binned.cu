@@ -238,8 +238,10 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
             }
         }
         if (staged) {
-            K* skp = sk + (s & (KA - 1));
-            VT* svp = sv + (s & (VA - 1));
+            // staging aligned like the destination modulo 16 bytes (the table
+            // arrays of a vertex-range slice start at any entry)
+            K* skp = sk + ((reinterpret_cast<uintptr_t>(okeys + s) / sizeof(K)) & (KA - 1));
+            VT* svp = sv + ((reinterpret_cast<uintptr_t>(ovals + s) / sizeof(VT)) & (VA - 1));
 #pragma unroll
             for (int k = 0; k < kItems; ++k) {
                 const uint32_t i = tid + k * kBuildBlock;

@@ -215,7 +215,7 @@ struct SplitLayout {
     static constexpr int kItems = split_items<E>();
     static constexpr int kTile = split_tile<E>();
     static constexpr size_t kInBytes = (size_t(kTile) * sizeof(InT) + 32 + 15) & ~size_t(15);
-    static constexpr size_t kBytes = kSplitStages * kInBytes + size_t(kTile) * (sizeof(E) + 1);
+    static constexpr size_t kBytes = kSplitStages * kInBytes + size_t(kTile) * sizeof(E) + kTile + 16;
 };
 
 // CTAs per SM the layout allows (<= 227 KB of shared memory per SM): 3 when
@@ -353,24 +353,34 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
         }
         if (lane == 31) s_wsum[warp] = inc;
         __syncthreads();
+        OffT gb = 0;
+        uint32_t off = 0;
         if (tid < ndig) {
             uint32_t base = 0;
             for (uint32_t w = 0; w < warp; ++w) base += s_wsum[w];
-            const uint32_t off = base + inc - c;
+            off = base + inc - c;
             s_off[tid] = off;
-            if (c) s_gbo[tid] = atom_add(cursor + cbase + tid, OffT(c)) - OffT(off);
+            // the run reservation is consumed only after the scatter below, so
+            // its L2 round trip overlaps the scatter
+            if (c) gb = atom_add(cursor + cbase + tid, OffT(c));
+            // digit of every slot of this digit's run, written by the digit's
+            // owner as a byte run (word stores in the middle) instead of one
+            // random byte store per entry in the scatter
+            uint32_t o = off;
+            const uint32_t e = off + c;
+            const uint8_t dd = uint8_t(tid);
+            while (o < e && (o & 3)) s_dig[o++] = dd;
+            const uint32_t w4 = uint32_t(dd) * 0x01010101u;
+            for (; o + 4 <= e; o += 4) *reinterpret_cast<uint32_t*>(s_dig + o) = w4;
+            while (o < e) s_dig[o++] = dd;
         }
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
             const uint32_t j = tid + k * kSplitBlock;
-            if (j < cnt) {
-                const uint32_t d = dr[k] >> 16;
-                const uint32_t slot = s_off[d] + (dr[k] & 0xFFFFu);
-                s_ent[slot] = ent[k];
-                s_dig[slot] = uint8_t(d);
-            }
+            if (j < cnt) s_ent[s_off[dr[k] >> 16] + (dr[k] & 0xFFFFu)] = ent[k];
         }
+        if (c) s_gbo[tid] = gb - OffT(off);
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
