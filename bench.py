@@ -38,7 +38,11 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--log2n", type=int, default=28)
+    p.add_argument("--log2n", type=int, default=None,
+                   help="c2: keys (and probes) per GPU, default 28; c5: TOTAL keys, default 32")
+    p.add_argument("--config", default="c2", choices=["c2", "c5"],
+                   help="c2: the BASELINE metric config (weak scaling, 2^28 per GPU); c5: "
+                        "2^32 keys + 2^32 probes in total split over the GPUs (strong scaling)")
     p.add_argument("--variant", type=int, default=2, choices=[1, 2])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
@@ -48,12 +52,33 @@ def parse():
                         "i.e. the same config)")
     p.add_argument("--csv", default="bench_rows.csv",
                    help="reference bench CSV rows (hashgraph_bench.cpp:47-49 + B200 columns)")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.log2n is None:
+        a.log2n = 32 if a.config == "c5" else 28
+    return a
 
 
-def workload_config(log2n: int, variant: int, world: int) -> dict:
-    """The `config` of both arms' JSON lines (identical for the same args)."""
+def per_gpu_log2n(args, world: int) -> int:
+    """log2 of the keys (= probes) each GPU holds."""
+    if args.config == "c5":
+        return args.log2n - (world.bit_length() - 1)
+    return args.log2n
+
+
+def workload_config(log2n: int, variant: int, world: int, config: str = "c2") -> dict:
+    """The `config` of both arms' JSON lines (identical for the same args);
+    log2n = keys per GPU."""
     n = 1 << log2n
+    if config == "c5":
+        tot = (1 << log2n) * world
+        return {"workload": f"C5: build_v{variant} over {tot} uniform u32 keys in total "
+                            f"(splitmix64 seed 1, global positions), load 1, hash-range sharded "
+                            f"over {world} GPU(s) + probe_standard (count) of {tot} u32 probes "
+                            f"(seed 2); strong scaling",
+                "n_total": tot, "m_total": tot, "n_per_gpu": n, "m_per_gpu": n,
+                "load_factor": 1.0, "variant": variant, "vertices": tot,
+                "l2": "inputs larger than L2",
+                "parallelism": f"hash-range shards x{world}" if world > 1 else "1 GPU"}
     return {"workload": f"C2: build_v{variant} over 2^{log2n} uniform u32 keys (splitmix64 "
                         f"seed 1) at load 1 + probe_standard (count) of 2^{log2n} u32 probes "
                         f"(seed 2), per GPU",
@@ -256,20 +281,22 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    log2n = args.cpu_log2n or args.log2n
+    own = per_gpu_log2n(args, world)
+    log2n = args.cpu_log2n or min(own, 28)
     steps = max(1, args.steps)
     # each step is a full 2^28 build + probe (~10-20 s on 16 cores): cap the
     # warm-up so K steps + W warm-ups end within a few minutes
     warm = min(args.warmup, 1)
     res = cpu_reference_rate(args.variant, log2n, steps, warm)
-    cfg = workload_config(args.log2n, args.variant, world)
+    cfg = workload_config(own, args.variant, world, args.config)
     line = {
         "impl": "reference", "metric": METRIC, "value": res["value"], "unit": "Gkeys/s",
         "n_gpus": args.gpus, "steps": steps, "warmup": warm,
-        "ms_per_step": res["seconds_median"] * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": res["seconds_median"] * 1e3, "higher_is_better": True,
+        "scaling": "strong" if args.config == "c5" else "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": cfg,
-        "same_config": log2n == args.log2n and world == 1,
+        "same_config": log2n == own and world == 1 and args.config == "c2",
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample",
                                               "cpu_model", "nproc", "library")},
         "e2e": {"value": res["value"], "unit": "Gkeys/s", "h2d_bytes_per_step": 0,
@@ -436,7 +463,11 @@ def run_b200(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    n = m = 1 << args.log2n
+    c5 = args.config == "c5"
+    if c5:  # the whole config is too large for the CPU arm and the pinned e2e copies
+        args.no_cpu = args.no_e2e = args.no_extras = True
+    log2n = per_gpu_log2n(args, world)
+    n = m = 1 << log2n
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
@@ -464,6 +495,8 @@ def run_b200(args):
         step()
     torch.cuda.synchronize()
     nv = hg.derived_vertex_count(n, 1.0)
+    if world > 1:
+        engine.exchange_events = []  # time the all-to-alls of the timed steps
 
     def barrier():
         if world > 1:
@@ -490,6 +523,22 @@ def run_b200(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = world * (n + m) / (ms * 1e-3) / 1e9
+    nvlink = None
+    if world > 1:
+        # NVLink 5 roofline of the exchanges: bytes this rank sends to other
+        # ranks per step (routed key records + probe keys) over the device
+        # time of its all-to-alls, against 900 GB/s per direction per GPU
+        xms = engine.exchange_ms() / args.steps
+        xb = int(engine.last_build_bytes + engine.last_probe_bytes)
+        t_ = torch.tensor([xms, float(xb)], device=dev, dtype=torch.float64)
+        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        xms_max, xb_max = float(t_[0]), float(t_[1])
+        nvlink = {"bytes_per_rank_per_step": xb, "exchange_ms_per_step": round(xms, 4),
+                  "achieved_gbs": round(xb / (xms * 1e-3) / 1e9, 1) if xms else None,
+                  "peak_gbs": 900.0, "peak_source": "NVLink 5, 900 GB/s per direction per GPU",
+                  "frac": round(xb / (xms * 1e-3) / 1e9 / 900.0, 4) if xms else None,
+                  "max_over_ranks": {"exchange_ms": round(xms_max, 4), "bytes": int(xb_max)},
+                  "exchange_share_of_step": round(xms / ms, 4)}
     matches, comparisons = (int(x) for x in result.cpu().tolist())
     gpu_launches = sum(l for (l, _) in kern.values())
 
@@ -528,10 +577,12 @@ def run_b200(args):
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "Gkeys/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "higher_is_better": True, "scaling": "strong" if c5 else "weak", "vs_baseline": None,
+        "dtype": "u32",
         "data": "synthetic",
-        "config": workload_config(args.log2n, args.variant, world),
+        "config": workload_config(log2n, args.variant, world, args.config),
         "roofline": roofline,
+        "nvlink": nvlink,
         "clocks": clocks.summary(),
         "gpu_launches": gpu_launches,
         "match_count": matches, "key_comparisons": comparisons,
@@ -679,13 +730,13 @@ def run_b200(args):
         # two trials (~30 s of CPU work), plus a 1-thread row on a 2^22 sample
         try:
             keys_ = ("value", "unit", "cores", "kind", "sample", "cpu_model", "nproc", "library")
-            cb = cpu_reference_rate(args.variant, args.cpu_log2n or args.log2n, trials=2, warmup=0)
+            cb = cpu_reference_rate(args.variant, args.cpu_log2n or log2n, trials=2, warmup=0)
             line["cpu_baseline"] = {k: cb[k] for k in keys_}
             c1 = cpu_reference_rate(args.variant, 22, trials=3, warmup=1, threads=1)
             line["cpu_baseline"]["threads_1"] = {k: c1[k] for k in ("value", "unit", "cores",
                                                                      "sample")}
             rows.append(csv_row("join", f"ref_hg_v{args.variant}+probe_standard", n, 1.0,
-                                cb["seconds_median"] * 1e3, 2 * (1 << (args.cpu_log2n or args.log2n)),
+                                cb["seconds_median"] * 1e3, 2 * (1 << (args.cpu_log2n or log2n)),
                                 trials=2, gpus=0, threads=cb["cores"]))
         except Exception as ex:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "error": str(ex)}

@@ -122,6 +122,12 @@ hg_status hg_table_device_arrays(const hg_table* t, const void** offsets, const 
 hg_status hg_table_export(const hg_table* t, uint64_t* offsets, uint64_t* keys, uint64_t* vals,
                           void* stream);
 
+/* hg_build from n AoS records {key, value} (the layout hg_route_records
+ * writes: 8-byte records for key_width = val_width = 4, else 16-byte records
+ * of two u64 fields); the binned build's first pass reads them directly. */
+hg_status hg_build_records(const void* records, int32_t key_width, int32_t val_width, uint64_t n,
+                           const hg_build_config* cfg, void* stream, hg_table** out);
+
 /* A device table from caller arrays in the reference layout (HashGraph's
  * constructor from offsets/edges, core.hpp:71-77): offsets[V+1], keys[N],
  * vals[N] as u64 (host or device). No validation is done here; hg_validate
@@ -231,6 +237,23 @@ hg_status hg_route(const void* keys, int32_t key_width, const void* vals, int32_
                    uint64_t n, uint64_t val_base, uint64_t hash_seed, int32_t hash_kind,
                    uint64_t global_vertices, uint32_t shards, void* out_keys, void* out_vals,
                    uint64_t* shard_counts, void* stream);
+
+/* hg_route with owner-grouped AoS records {key, value} in ONE device buffer
+ * (8-byte records for key_width = val_width = 4, else 16-byte records with
+ * both fields widened to u64) -- the one buffer a single all-to-all moves and
+ * hg_build_records consumes. shard_counts: device, G entries. */
+hg_status hg_route_records(const void* keys, int32_t key_width, const void* vals,
+                           int32_t val_width, uint64_t n, uint64_t val_base, uint64_t hash_seed,
+                           int32_t hash_kind, uint64_t global_vertices, uint32_t shards,
+                           void* out_records, uint64_t* shard_counts, void* stream);
+
+/* Groups n match pairs (left[i], right[i]) (pair_width 4 or 8, device) by
+ * owner = right[i] / span into AoS records {left, right} (device), G <= 256
+ * -- the reverse routing that returns pairs to the rank holding each probe
+ * (probes of rank r have global positions [r * span, (r + 1) * span)). */
+hg_status hg_route_pairs(const void* left, const void* right, int32_t pair_width, uint64_t n,
+                         uint64_t span, uint32_t shards, void* out_records, uint64_t* shard_counts,
+                         void* stream);
 
 /* Synthetic inputs: kind 0 = (u32|u64)splitmix64(seed, start+i);
  * kind 1 = C4 probes with hit ratio `hit` over ref[n_ref]; kind 2 = scramble31(start+i);

@@ -111,6 +111,11 @@ SIGNATURES = {
                             C.POINTER(hg_probe_options), C.POINTER(hg_probe_result), _vp]),
     "hg_count_instances": (_i32, [_vp, _u64, C.POINTER(_u64), _vp]),
     "hg_validate": (_i32, [_vp, _vp, _u64, C.POINTER(_i32), _vp]),
+    "hg_route_records": (_i32, [_vp, _i32, _vp, _i32, _u64, _u64, _u64, _i32, _u64, C.c_uint32,
+                                _vp, _vp, _vp]),
+    "hg_route_pairs": (_i32, [_vp, _vp, _i32, _u64, _u64, C.c_uint32, _vp, _vp, _vp]),
+    "hg_build_records": (_i32, [_vp, _i32, _i32, _u64, C.POINTER(hg_build_config), _vp,
+                                C.POINTER(_vp)]),
     "hg_count_instances_hasher": (_i32, [_vp, _u64, _i32, _u64, C.POINTER(_u64), _vp]),
     "hg_validate_hasher": (_i32, [_vp, _vp, _u64, _i32, _u64, C.POINTER(_i32), _vp]),
     "hg_generate": (_i32, [_vp, _i32, _u64, _i32, _u64, _u64, C.c_double, _vp, _u64, _vp]),

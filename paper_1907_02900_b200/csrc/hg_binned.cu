@@ -504,7 +504,8 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
         if ((e = cudaMemsetAsync(ticket, 0, 8, s)) != cudaSuccess) break;  // ticket, big_n
         e = partition<K, VT, OffT, POW2>(static_cast<const K*>(a.keys),
                                          static_cast<const VT*>(a.vals), t.n, t.seed, t.hash_kind,
-                                         nv, g, part_start, pscratch, reorg, s, kBuildPassNames);
+                                         nv, g, part_start, pscratch, reorg, s, kBuildPassNames,
+                                         static_cast<const E*>(a.records));
         if (e != cudaSuccess) break;
         auto kb = k_part_build<K, VT, OffT, POW2>;
         if ((e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize,

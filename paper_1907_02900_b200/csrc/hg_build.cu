@@ -313,9 +313,10 @@ static uint32_t v2_slice_shift(const TableDesc& t, const BuildArgs& a, size_t en
 // Binned build over a vertex range wider than 2^16 partitions of the tuned
 // width (V > 2^28 at load 1, e.g. 2^31 keys or C5's 2^31-vertex shards). The
 // reference's bin split (core.hpp:192-197) is applied once more on top: K11
-// routes the keys into G slices of 2^sshift consecutive vertices (SoA keys +
-// input positions, hg_shard.cu), then each slice is built by the binned build
-// into its range of the one table -- offsets written with the slice's entry
+// routes the keys into G slices of 2^sshift consecutive vertices as AoS
+// records {key, input position} (hg_shard.cu), then each slice is built by
+// the binned build (whose first pass reads the records) into its range of
+// the one table -- offsets written with the slice's entry
 // base (TableDesc::obase), keys / values at the slice's entry range -- so
 // every slice keeps the tuned partition geometry (two 8-bit digits, K7 at two
 // CTAs per SM). Extra traffic: one routing pass, N (kb + vb) read + written.
@@ -325,19 +326,20 @@ static cudaError_t build_v2_sliced(const TableDesc& t, const BuildArgs& a, uint3
     const uint64_t S = uint64_t(1) << sshift;
     const uint64_t G = (t.nv + S - 1) / S;
     if (G > 256) return cudaErrorInvalidValue;
-    const size_t kbytes = (t.n * sizeof(K) + 255) & ~size_t(255);
-    const size_t vbytes = (t.n * sizeof(VT) + 255) & ~size_t(255);
+    using E = typename EntryT<K, VT>::T;
+    const size_t rbytes = (t.n * sizeof(E) + 255) & ~size_t(255);
     char* scratch = nullptr;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), kbytes + vbytes + 256 * 8, s);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), rbytes + 256 * 8, s);
     if (e != cudaSuccess) return e;
-    K* rk = reinterpret_cast<K*>(scratch);
-    VT* rv = reinterpret_cast<VT*>(scratch + kbytes);
-    uint64_t* dcnt = reinterpret_cast<uint64_t*>(scratch + kbytes + vbytes);
+    E* rec = reinterpret_cast<E*>(scratch);
+    uint64_t* dcnt = reinterpret_cast<uint64_t*>(scratch + rbytes);
     uint64_t cnt[256];
     do {
+        // slices as AoS records {key, input position}: each slice's binned
+        // build reads them directly in its first pass
         if ((e = route_keys(a.keys, sizeof(K), a.vals, sizeof(VT), t.n, 0, t.seed, t.hash_kind,
-                            global_nv(t), t.vbase, t.nv, S, uint32_t(G), rk, rv, dcnt, s)) !=
-            cudaSuccess)
+                            global_nv(t), t.vbase, t.nv, S, uint32_t(G), nullptr, nullptr, dcnt, s,
+                            rec)) != cudaSuccess)
             break;
         if ((e = cudaMemcpyAsync(cnt, dcnt, G * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
             (e = cudaStreamSynchronize(s)) != cudaSuccess)
@@ -354,8 +356,9 @@ static cudaError_t build_v2_sliced(const TableDesc& t, const BuildArgs& a, uint3
             sub.keys = static_cast<K*>(t.keys) + start;
             sub.vals = static_cast<VT*>(t.vals) + start;
             BuildArgs sa = a;
-            sa.keys = rk + start;
-            sa.vals = rv + start;
+            sa.keys = nullptr;
+            sa.vals = nullptr;
+            sa.records = rec + start;
             sa.n = cnt[g];
             sa.stable = 0;
             e = build_v2_impl<K, VT, OffT, HM>(sub, sa, s);
@@ -366,9 +369,50 @@ static cudaError_t build_v2_sliced(const TableDesc& t, const BuildArgs& a, uint3
     return e;
 }
 
+// AoS records -> SoA keys / values (the simple build and the sliced binned
+// build take SoA input; the binned build's first pass reads records directly).
+template <typename K, typename VT>
+__global__ void k_unpack_records(const typename EntryT<K, VT>::T* __restrict__ rec, uint64_t n,
+                                 K* __restrict__ keys, VT* __restrict__ vals) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const auto r = rec[i];
+        keys[i] = EntryT<K, VT>::key(r);
+        vals[i] = EntryT<K, VT>::val(r);
+    }
+}
+
+template <typename K, typename VT, typename OffT>
+static cudaError_t build_typed(const TableDesc& t, const BuildArgs& a, cudaStream_t s);
+
+template <typename K, typename VT, typename OffT>
+static cudaError_t build_from_records_soa(const TableDesc& t, const BuildArgs& a, cudaStream_t s) {
+    const size_t kb = (t.n * sizeof(K) + 255) & ~size_t(255);
+    char* scr = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scr), kb + t.n * sizeof(VT) + 256, s);
+    if (e != cudaSuccess) return e;
+    K* keys = reinterpret_cast<K*>(scr);
+    VT* vals = reinterpret_cast<VT*>(scr + kb);
+    k_unpack_records<K, VT><<<unsigned(std::min<uint64_t>((t.n + 255) / 256, uint64_t(num_sms()) * 16)),
+                              256, 0, s>>>(static_cast<const typename EntryT<K, VT>::T*>(a.records),
+                                           t.n, keys, vals);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) {
+        BuildArgs b = a;
+        b.records = nullptr;
+        b.keys = keys;
+        b.vals = vals;
+        e = build_typed<K, VT, OffT>(t, b, s);
+    }
+    cudaFreeAsync(scr, s);
+    return e;
+}
+
 template <typename K, typename VT, typename OffT>
 static cudaError_t build_typed(const TableDesc& t, const BuildArgs& a, cudaStream_t s) {
     const uint32_t sshift = a.variant == 2 ? v2_slice_shift(t, a, sizeof(typename EntryT<K, VT>::T)) : 0;
+    if (a.records && t.n && (a.variant != 2 || sshift))
+        return build_from_records_soa<K, VT, OffT>(t, a, s);
     cudaError_t e = dispatch_hash_mode(hash_mode(global_nv(t), t.hash_kind), [&](auto hm) {
         constexpr int HM = decltype(hm)::value;
         if (sshift) return build_v2_sliced<K, VT, OffT, HM>(t, a, sshift, s);

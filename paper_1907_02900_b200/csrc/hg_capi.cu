@@ -207,8 +207,12 @@ uint64_t hg_hash_to_vertex(uint64_t key, uint64_t seed, uint64_t nv) {
     return x % nv;
 }
 
-hg_status hg_build(const void* keys, int32_t key_width, const void* vals, int32_t val_width,
-                   uint64_t n, const hg_build_config* cfg_in, void* stream, hg_table** out) {
+// hg_build / hg_build_records: keys + optional values (SoA), or n AoS
+// records {key, value} (key_width / val_width each, 8-byte records for
+// 4 + 4, else 16 with both fields widened to 8 bytes).
+static hg_status build_common(const void* keys, int32_t key_width, const void* vals,
+                              int32_t val_width, const void* records, uint64_t n,
+                              const hg_build_config* cfg_in, void* stream, hg_table** out) {
     if (!out) return fail(HG_EINVAL, "out is NULL");
     *out = nullptr;
     hg_build_config cfg;
@@ -221,12 +225,13 @@ hg_status hg_build(const void* keys, int32_t key_width, const void* vals, int32_
     if (!(cfg.load_factor > 0.0)) return fail(HG_EINVAL, "load_factor must be positive");
     if (cfg.bin_count < 1) return fail(HG_EINVAL, "bin_count must be at least 1");
     if (key_width != 4 && key_width != 8) return fail(HG_EINVAL, "key_width must be 4 or 8");
-    if (vals && val_width != 4 && val_width != 8) return fail(HG_EINVAL, "val_width must be 4 or 8");
+    if ((vals || records) && val_width != 4 && val_width != 8)
+        return fail(HG_EINVAL, "val_width must be 4 or 8");
     if (cfg.variant != HG_BUILD_SIMPLE && cfg.variant != HG_BUILD_BINNED)
         return fail(HG_EINVAL, "variant must be 1 (simple) or 2 (binned)");
     if (cfg.hash_kind != HG_HASH_MIX64 && cfg.hash_kind != HG_HASH_IDENTITY)
         return fail(HG_EINVAL, "unknown hash_kind");
-    if (n && !keys) return fail(HG_EINVAL, "keys is NULL");
+    if (n && !keys && !records) return fail(HG_EINVAL, "keys is NULL");
     uint64_t nv = cfg.vertex_count;
     if (cfg.global_vertices) {
         if (!nv) return fail(HG_EINVAL, "a shard build needs vertex_count (its local vertex range)");
@@ -252,7 +257,7 @@ hg_status hg_build(const void* keys, int32_t key_width, const void* vals, int32_
     d.seed = cfg.hash_seed;
     d.hash_kind = cfg.hash_kind;
     d.key_bytes = key_width;
-    d.val_bytes = vals ? val_width : (n <= (uint64_t(1) << 32) ? 4 : 8);
+    d.val_bytes = (vals || records) ? val_width : (n <= (uint64_t(1) << 32) ? 4 : 8);
     d.off_bytes = (n < (uint64_t(1) << 32) && nv <= (uint64_t(1) << 32)) ? 4 : 8;
     // offs is padded so that offs + 1 (the counter / cursor view) is 16-byte aligned.
     const uint64_t pad = 16 / d.off_bytes - 1;
@@ -266,12 +271,14 @@ hg_status hg_build(const void* keys, int32_t key_width, const void* vals, int32_
     d.offs = static_cast<char*>(t->alloc_offs) + pad * d.off_bytes;
 
     DevIn kin, vin;
-    e = kin.stage(keys, n * key_width, s);
-    if (e == cudaSuccess && vals) e = vin.stage(vals, n * val_width, s);
+    const uint64_t rec_bytes = (key_width == 4 && val_width == 4) ? 8 : 16;
+    e = records ? kin.stage(records, n * rec_bytes, s) : kin.stage(keys, n * key_width, s);
+    if (e == cudaSuccess && vals && !records) e = vin.stage(vals, n * val_width, s);
     if (e == cudaSuccess) {
         hg::BuildArgs a;
-        a.keys = kin.ptr;
-        a.vals = vals ? vin.ptr : nullptr;
+        a.keys = records ? nullptr : kin.ptr;
+        a.vals = vals && !records ? vin.ptr : nullptr;
+        a.records = records ? kin.ptr : nullptr;
         a.n = n;
         a.variant = cfg.variant;
         a.aggregate = cfg.aggregate < 0 ? 1 : cfg.aggregate;
@@ -287,6 +294,17 @@ hg_status hg_build(const void* keys, int32_t key_width, const void* vals, int32_
     }
     *out = t;
     return HG_OK;
+}
+
+hg_status hg_build(const void* keys, int32_t key_width, const void* vals, int32_t val_width,
+                   uint64_t n, const hg_build_config* cfg, void* stream, hg_table** out) {
+    return build_common(keys, key_width, vals, val_width, nullptr, n, cfg, stream, out);
+}
+
+hg_status hg_build_records(const void* records, int32_t key_width, int32_t val_width, uint64_t n,
+                           const hg_build_config* cfg, void* stream, hg_table** out) {
+    if (n && !records) return fail(HG_EINVAL, "records is NULL");
+    return build_common(nullptr, key_width, nullptr, val_width, records, n, cfg, stream, out);
 }
 
 hg_status hg_table_import(const uint64_t* offsets, const uint64_t* keys, const uint64_t* vals,
@@ -809,6 +827,48 @@ hg_status hg_route(const void* keys, int32_t key_width, const void* vals, int32_
     }
     if (!counts_dev) cudaFreeAsync(dc, s);
     if (e != cudaSuccess) return cuda_fail(e, "hg_route");
+    return HG_OK;
+}
+
+hg_status hg_route_records(const void* keys, int32_t key_width, const void* vals,
+                           int32_t val_width, uint64_t n, uint64_t val_base, uint64_t hash_seed,
+                           int32_t hash_kind, uint64_t global_vertices, uint32_t shards,
+                           void* out_records, uint64_t* shard_counts, void* stream) {
+    if (key_width != 4 && key_width != 8) return fail(HG_EINVAL, "key_width must be 4 or 8");
+    if (val_width != 4 && val_width != 8) return fail(HG_EINVAL, "val_width must be 4 or 8");
+    if (shards < 1 || shards > 256) return fail(HG_EINVAL, "shards must be in [1, 256]");
+    if (global_vertices < 1) return fail(HG_EINVAL, "global_vertices must be >= 1");
+    if (hash_kind != HG_HASH_MIX64 && hash_kind != HG_HASH_IDENTITY)
+        return fail(HG_EINVAL, "unknown hash_kind");
+    if (!shard_counts || !is_device_ptr(shard_counts))
+        return fail(HG_EINVAL, "shard_counts must be a device buffer");
+    if (n && (!is_device_ptr(keys) || !is_device_ptr(out_records) || (vals && !is_device_ptr(vals))))
+        return fail(HG_EINVAL, "hg_route_records takes device buffers");
+    int dev = 0;
+    if (hg_status st = need_device(&dev); st != HG_OK) return st;
+    cudaError_t e = hg::route_keys(keys, key_width, vals, val_width, n, val_base, hash_seed,
+                                   hash_kind, global_vertices, 0, global_vertices, 0, shards,
+                                   nullptr, nullptr, shard_counts, static_cast<cudaStream_t>(stream),
+                                   out_records);
+    if (e != cudaSuccess) return cuda_fail(e, "hg_route_records");
+    return HG_OK;
+}
+
+hg_status hg_route_pairs(const void* left, const void* right, int32_t pair_width, uint64_t n,
+                         uint64_t span, uint32_t shards, void* out_records, uint64_t* shard_counts,
+                         void* stream) {
+    if (pair_width != 4 && pair_width != 8) return fail(HG_EINVAL, "pair_width must be 4 or 8");
+    if (shards < 1 || shards > 256) return fail(HG_EINVAL, "shards must be in [1, 256]");
+    if (span < 1) return fail(HG_EINVAL, "span must be >= 1");
+    if (!shard_counts || !is_device_ptr(shard_counts))
+        return fail(HG_EINVAL, "shard_counts must be a device buffer");
+    if (n && (!is_device_ptr(left) || !is_device_ptr(right) || !is_device_ptr(out_records)))
+        return fail(HG_EINVAL, "hg_route_pairs takes device buffers");
+    int dev = 0;
+    if (hg_status st = need_device(&dev); st != HG_OK) return st;
+    cudaError_t e = hg::route_pairs(left, right, pair_width, n, span, shards, out_records,
+                                    shard_counts, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "hg_route_pairs");
     return HG_OK;
 }
 

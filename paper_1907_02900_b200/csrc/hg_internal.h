@@ -36,6 +36,9 @@ struct BuildArgs {
     int aggregate = 1;           // warp-aggregated atomics
     int stable = 0;              // reproduce ExecMode::sequential segment order
     uint64_t partition_vertices = 0;  // V2 partition width (0 = auto)
+    // non-null: the input is n AoS records {key, value} (EntryT<K, VT>::T,
+    // routed by route_keys with out_records) instead of keys / vals
+    const void* records = nullptr;
 };
 
 // Builds into t (offs/keys/vals already allocated). Scratch is allocated
@@ -55,6 +58,10 @@ struct ProbeArgs {
     uint64_t cap = 0;
     uint64_t* pair_offsets = nullptr;
     int method = 0;                // 0 auto, 1 direct gathers, 2 partitioned
+    // partitioned probe only: m AoS records {key, original probe position}
+    // (EntryT<K, u32 | u64>::T, route_keys with out_records) instead of
+    // `probes`; per-probe counts land at the original positions
+    const void* records = nullptr;
 };
 
 cudaError_t probe_table(const TableDesc& t, const ProbeArgs& a, cudaStream_t s);
@@ -102,7 +109,15 @@ cudaError_t route_keys(const void* keys, int key_bytes, const void* vals, int va
                        uint64_t n, uint64_t val_base, uint64_t seed, int hash_kind,
                        uint64_t global_vertices, uint64_t vertex_base, uint64_t local_vertices,
                        uint64_t span, uint32_t shards, void* out_keys, void* out_vals,
-                       uint64_t* shard_counts, cudaStream_t s);
+                       uint64_t* shard_counts, cudaStream_t s, void* out_records = nullptr);
+
+// As route_keys with out_records != nullptr: owner-grouped AoS records
+// {key, value} (EntryT<K, VT>::T: 8 bytes for u32/u32, else 16) instead of SoA.
+// route_pairs: groups match pairs (left[i], right[i]) by owner = right / span
+// into AoS records of 2 x pair_bytes (pairs returned to the probe's rank).
+cudaError_t route_pairs(const void* left, const void* right, int pair_bytes, uint64_t n,
+                        uint64_t span, uint32_t shards, void* out_records, uint64_t* shard_counts,
+                        cudaStream_t s);
 
 // Kernel timeline hooks (hg_prof.cu).
 bool prof_enabled();

@@ -838,7 +838,8 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
         if (need_idx) {
             e = partition<K, IT, OffT, POW2>(probes, static_cast<const IT*>(nullptr), a.m, t.seed,
                                              t.hash_kind, nv, g, ppart, pscratch,
-                                             static_cast<E1*>(reorg), s, kProbePassNames);
+                                             static_cast<E1*>(reorg), s, kProbePassNames,
+                                             static_cast<const E1*>(a.records));
         } else {
             e = partition<K, void, OffT, POW2>(probes, static_cast<const void*>(nullptr), a.m,
                                                t.seed, t.hash_kind, nv, g, ppart, pscratch,
@@ -952,6 +953,61 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
     return e;
 }
 
+// Tables whose vertex range is too wide for the partitioned probe (its
+// offsets slice must fit shared memory within 2^16 partitions: V > 2^30 at
+// load 1, e.g. 2^31-key tables or C5's 2^32 vertices on one GPU): the probes
+// are routed into power-of-two vertex-range slices first (K11, hg_shard.cu;
+// keys only when counting, records {key, probe position} for per-probe
+// counts) and each slice is probed by the partitioned probe against its
+// view of the table (offsets of the slice's range, global entry positions).
+template <typename K, typename VT, typename OffT, typename IT, int POW2>
+static cudaError_t probe_sliced(const TableDesc& t, const ProbeArgs& a, uint32_t sshift,
+                                cudaStream_t s) {
+    using E = typename EntryT<K, IT>::T;
+    const uint64_t S = uint64_t(1) << sshift;
+    const uint64_t G = (t.nv + S - 1) / S;
+    if (G > 256) return cudaErrorInvalidValue;
+    const bool idx = a.counts != nullptr && a.counts_requested;
+    const size_t bytes = (a.m * (idx ? sizeof(E) : sizeof(K)) + 255) & ~size_t(255);
+    char* scratch = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes + 256 * 8, s);
+    if (e != cudaSuccess) return e;
+    uint64_t* dcnt = reinterpret_cast<uint64_t*>(scratch + bytes);
+    uint64_t cnt[256];
+    do {
+        e = route_keys(a.probes, sizeof(K), nullptr, sizeof(IT), a.m, 0, t.seed, t.hash_kind,
+                       global_nv(t), t.vbase, t.nv, S, uint32_t(G), idx ? nullptr : scratch,
+                       nullptr, dcnt, s, idx ? scratch : nullptr);
+        if (e != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(cnt, dcnt, G * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+            (e = cudaStreamSynchronize(s)) != cudaSuccess)
+            break;
+        uint64_t start = 0;
+        for (uint64_t g = 0; g < G && e == cudaSuccess; ++g) {
+            TableDesc sub = t;
+            sub.nv = t.nv - g * S < S ? t.nv - g * S : S;
+            sub.gnv = global_nv(t);
+            sub.vbase = t.vbase + g * S;
+            sub.offs = static_cast<OffT*>(t.offs) + g * S;  // global entry positions
+            sub.n = uint64_t(double(t.n) * double(sub.nv) / double(t.nv));  // density estimate
+            ProbeArgs sa = a;
+            sa.m = cnt[g];
+            sa.method = 2;
+            if (idx) {
+                sa.probes = nullptr;
+                sa.records = reinterpret_cast<const E*>(scratch) + start;
+            } else {
+                sa.probes = reinterpret_cast<const K*>(scratch) + start;
+                sa.counts = nullptr;
+            }
+            if (sa.m) e = probe_partitioned<K, VT, OffT, IT, POW2>(sub, sa, s);
+            start += cnt[g];
+        }
+    } while (false);
+    cudaFreeAsync(scratch, s);
+    return e;
+}
+
 template <typename K, typename VT, typename OffT, int POW2>
 static cudaError_t probe_impl(const TableDesc& t, const ProbeArgs& a, cudaStream_t s) {
     const Divisor nv = make_divisor(global_nv(t), t.vbase);
@@ -972,6 +1028,18 @@ static cudaError_t probe_impl(const TableDesc& t, const ProbeArgs& a, cudaStream
         if (a.m <= (uint64_t(1) << 32))
             return probe_partitioned<K, VT, OffT, uint32_t, POW2>(t, a, s);
         return probe_partitioned<K, VT, OffT, uint64_t, POW2>(t, a, s);
+    }
+    // too wide for one partitioned pass: slices of 2^(16 + ps) vertices, ps the
+    // widest partition whose offsets slice fits (count-only / per-probe counts)
+    if (!fits && !a.pairs && a.method != 1 && table_bytes > (uint64_t(96) << 20) &&
+        a.m >= (uint64_t(1) << 20)) {
+        const double per_vertex = double(t.n) / double(t.nv);
+        uint32_t ps = 0;  // make_geom's natural width (~4096 entries per partition)
+        while (ps < kMaxPartShift && per_vertex * double(uint64_t(2) << ps) <= 4096.0) ++ps;
+        while (ps > 0 && (size_t(1) << ps) * sizeof(OffT) > size_t(64) << 10) --ps;
+        if (a.m <= (uint64_t(1) << 32))
+            return probe_sliced<K, VT, OffT, uint32_t, POW2>(t, a, 16 + ps, s);
+        return probe_sliced<K, VT, OffT, uint64_t, POW2>(t, a, 16 + ps, s);
     }
     const int sms = num_sms();
     const bool need_counts = a.counts != nullptr;

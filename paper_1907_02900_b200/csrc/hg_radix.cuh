@@ -116,17 +116,28 @@ inline PartGeom make_geom(uint64_t nv, uint64_t n, uint64_t want_pv, double targ
 
 constexpr int kHistBlock = 1024;
 
-template <typename K, typename OffT, int POW2>
+// In = K (raw keys) or a record type {key, value} (uint2 / ulonglong2: routed
+// records of a sharded build, hg_build_records); the key is its first field.
+template <typename K, typename In>
+__device__ __forceinline__ K key_of(const In& x) {
+    if constexpr (std::is_same<In, K>::value) {
+        return x;
+    } else {
+        return K(x.x);
+    }
+}
+
+template <typename K, typename OffT, int POW2, typename In = K>
 __global__ void __launch_bounds__(kHistBlock)
-k_part_hist(const K* __restrict__ keys, uint64_t n, uint64_t seed, int hk, Divisor nv,
+k_part_hist(const In* __restrict__ keys, uint64_t n, uint64_t seed, int hk, Divisor nv,
             uint32_t pshift, uint32_t nparts, OffT* __restrict__ hist) {
     extern __shared__ uint32_t sh[];  // nparts/2 words, two 16-bit counters each
     const uint32_t words = (nparts + 1) >> 1;
     for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) sh[i] = 0;
     __syncthreads();
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-    constexpr int VEC = 16 / sizeof(K);
-    using V = typename std::conditional<sizeof(K) == 4, uint4, ulonglong2>::type;
+    constexpr int VEC = 16 / sizeof(In);
+    using V = typename std::conditional<sizeof(In) == 4, uint4, ulonglong2>::type;
     auto count = [&](K key) {
         const uint32_t p = uint32_t(hv<POW2>(key, seed, hk, nv) >> pshift);
         const uint32_t sft = (p & 1) << 4;
@@ -137,10 +148,10 @@ k_part_hist(const K* __restrict__ keys, uint64_t n, uint64_t seed, int hk, Divis
             red_add(hist + p, OffT(0x8000));
         }
     };
-    uint64_t head = ((16 - (reinterpret_cast<uintptr_t>(keys) & 15)) & 15) / sizeof(K);
+    uint64_t head = ((16 - (reinterpret_cast<uintptr_t>(keys) & 15)) & 15) / sizeof(In);
     if (head > n) head = n;
     const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (gtid < head) count(keys[gtid]);
+    if (gtid < head) count(key_of<K>(keys[gtid]));
     const uint64_t nvec = (n - head) / VEC;
     const V* body = reinterpret_cast<const V*>(keys + head);
     // two 16-byte vectors per step, software-pipelined one step ahead so the
@@ -161,24 +172,24 @@ k_part_hist(const K* __restrict__ keys, uint64_t n, uint64_t seed, int hk, Divis
                 a = __ldcs(body + q + 2 * st);
                 b = __ldcs(body + q + 3 * st);
             }
-            const K* ka = reinterpret_cast<const K*>(&ca);
-            const K* kb = reinterpret_cast<const K*>(&cb);
+            const In* ka = reinterpret_cast<const In*>(&ca);
+            const In* kb = reinterpret_cast<const In*>(&cb);
 #pragma unroll
-            for (int k = 0; k < VEC; ++k) count(ka[k]);
+            for (int k = 0; k < VEC; ++k) count(key_of<K>(ka[k]));
 #pragma unroll
-            for (int k = 0; k < VEC; ++k) count(kb[k]);
+            for (int k = 0; k < VEC; ++k) count(key_of<K>(kb[k]));
         }
         if (q < nv_) {
             const V a1 = __ldcs(body + q);
-            const K* ka = reinterpret_cast<const K*>(&a1);
+            const In* ka = reinterpret_cast<const In*>(&a1);
 #pragma unroll
-            for (int k = 0; k < VEC; ++k) count(ka[k]);
+            for (int k = 0; k < VEC; ++k) count(key_of<K>(ka[k]));
         }
     };
     if (nvec + 4 * stride < (uint64_t(1) << 32)) sweep(uint32_t(0));
     else sweep(uint64_t(0));
     const uint64_t done = head + nvec * VEC;
-    if (gtid < n - done) count(keys[done + gtid]);
+    if (gtid < n - done) count(key_of<K>(keys[done + gtid]));
     __syncthreads();
     for (uint32_t p = threadIdx.x; p < nparts; p += blockDim.x) {
         const uint32_t c = (sh[p >> 1] >> ((p & 1) << 4)) & 0xFFFFu;
@@ -440,7 +451,8 @@ struct PartitionScratch {
 template <typename K, typename VT, typename OffT, int POW2>
 cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, int hk,
                       const Divisor& nv, const PartGeom& g, OffT* part_start, void* scratch,
-                      typename EntryT<K, VT>::T* out, cudaStream_t s, const char* const names[3]) {
+                      typename EntryT<K, VT>::T* out, cudaStream_t s, const char* const names[3],
+                      const typename EntryT<K, VT>::T* rec = nullptr) {
     using PS = PartitionScratch<K, VT, OffT>;
     using E = typename EntryT<K, VT>::T;
     char* p = static_cast<char*>(scratch);
@@ -460,19 +472,28 @@ cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, 
     if (e != cudaSuccess) return e;
     const int sms = num_sms();
     const size_t hsmem = ((g.nparts + 1) / 2) * 4;
-    auto kh = k_part_hist<K, OffT, POW2>;
-    if (hsmem > 48 * 1024 &&
-        (e = cudaFuncSetAttribute(kh, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hsmem))) !=
-            cudaSuccess)
-        return e;
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kh, kHistBlock, hsmem);
-    unsigned grid = unsigned(std::max(1, per_sm) * sms);
-    grid = unsigned(std::max<uint64_t>(
-        1, std::min<uint64_t>(grid, (n + kHistBlock * 16 - 1) / (kHistBlock * 16))));
-    HG_LAUNCH(names[0], s, kh<<<grid, kHistBlock, hsmem, s>>>(keys, n, seed, hk, nv, g.pshift,
-                                                        uint32_t(g.nparts), hist));
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    auto launch_hist = [&](auto kh, const auto* in) -> cudaError_t {
+        cudaError_t r;
+        if (hsmem > 48 * 1024 &&
+            (r = cudaFuncSetAttribute(kh, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hsmem))) !=
+                cudaSuccess)
+            return r;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kh, kHistBlock, hsmem);
+        unsigned grid = unsigned(std::max(1, per_sm) * sms);
+        grid = unsigned(std::max<uint64_t>(
+            1, std::min<uint64_t>(grid, (n + kHistBlock * 16 - 1) / (kHistBlock * 16))));
+        HG_LAUNCH(names[0], s, kh<<<grid, kHistBlock, hsmem, s>>>(in, n, seed, hk, nv, g.pshift,
+                                                            uint32_t(g.nparts), hist));
+        return cudaGetLastError();
+    };
+    if constexpr (EntryT<K, VT>::kHasVal) {
+        e = rec ? launch_hist(k_part_hist<K, OffT, POW2, E>, rec)
+                : launch_hist(k_part_hist<K, OffT, POW2>, keys);
+    } else {
+        e = launch_hist(k_part_hist<K, OffT, POW2>, keys);
+    }
+    if (e != cudaSuccess) return e;
     if ((e = launch_scan<OffT, OffT>(hist, part_start, g.nparts, scan_scr, part_start + g.nparts, s,
                                      "part_scan")) != cudaSuccess)
         return e;
@@ -482,10 +503,13 @@ cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, 
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     constexpr int kSplitTile = split_tile<E>();
     const uint64_t tiles1 = (n + kSplitTile - 1) / kSplitTile;
-    auto ks1 = k_multisplit<K, VT, OffT, true, false, POW2>;
+    // pass 1 reads the raw keys (+ values), or routed records (entries already)
+    auto ks1 = rec ? k_multisplit<K, VT, OffT, false, false, POW2>
+                   : k_multisplit<K, VT, OffT, true, false, POW2>;
     auto ks2 = k_multisplit<K, VT, OffT, false, true, POW2>;
-    constexpr size_t sm1 = SplitLayout<K, VT, true>::kBytes;
+    const size_t sm1 = rec ? SplitLayout<K, VT, false>::kBytes : SplitLayout<K, VT, true>::kBytes;
     constexpr size_t sm2 = SplitLayout<K, VT, false>::kBytes;
+    const void* in1 = rec ? static_cast<const void*>(rec) : static_cast<const void*>(keys);
     if ((e = cudaFuncSetAttribute(ks1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm1))) !=
             cudaSuccess ||
         (e = cudaFuncSetAttribute(ks2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm2))) !=
@@ -502,13 +526,13 @@ cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, 
         // single pass straight into partition order
         HG_LAUNCH(names[1], s,
                   (ks1<<<g1, kSplitBlock, sm1, s>>>(
-                      keys, vals, n, seed, hk, nv, g.pshift, 0, uint32_t((1u << g.b1) - 1), 0,
+                      in1, vals, n, seed, hk, nv, g.pshift, 0, uint32_t((1u << g.b1) - 1), 0,
                       cur2, part_start, 0, nullptr, tiles1, g.nparts, out)));
         return cudaGetLastError();
     }
     HG_LAUNCH(names[1], s,
               (ks1<<<g1, kSplitBlock, sm1, s>>>(
-                  keys, vals, n, seed, hk, nv, g.pshift, g.b2, uint32_t((1u << g.b1) - 1), 0, cur1,
+                  in1, vals, n, seed, hk, nv, g.pshift, g.b2, uint32_t((1u << g.b1) - 1), 0, cur1,
                   part_start, 0, nullptr, tiles1, g.nparts, mid)));
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     k_tile_prefix<OffT><<<1, 32, 0, s>>>(part_start, g.nparts, nb1, g.b2, kSplitTile, tile_prefix);

@@ -16,6 +16,7 @@
 
 #include "hg_common.cuh"
 #include "hg_internal.h"
+#include "hg_radix.cuh"
 #include "hg_scan.cuh"
 
 namespace hg {
@@ -24,34 +25,47 @@ constexpr int kRouteBlock = 512;
 constexpr int kRouteItems = 4;
 constexpr int kRouteTile = kRouteBlock * kRouteItems;
 
+// Owner of an item: its key's hash range (build / probe routing: owner =
+// ((h(key) mod V) - vertex_base) / span) or its value's range (match pairs
+// returned to the rank holding the probe: owner = value / span).
 template <int POW2>
-__device__ __forceinline__ uint32_t owner_of(uint64_t key, uint64_t seed, int hk, const Divisor& gv,
-                                             const Divisor& span) {
-    const uint64_t v = vhash<POW2>(key, seed, gv);
-    return uint32_t(div_of<false>(v, span));
-}
+struct OwnHash {
+    uint64_t seed;
+    Divisor gv, span;
+    __device__ __forceinline__ uint32_t operator()(uint64_t key, uint64_t) const {
+        return uint32_t(div_of<false>(vhash<POW2>(key, seed, gv), span));
+    }
+};
+struct OwnVal {
+    Divisor span;
+    __device__ __forceinline__ uint32_t operator()(uint64_t, uint64_t val) const {
+        return uint32_t(div_of<false>(val, span));
+    }
+};
 
-template <typename K, int POW2>
+template <typename K, typename VT, typename Own>
 __global__ void __launch_bounds__(kRouteBlock)
-k_route_hist(const K* __restrict__ keys, uint64_t n, uint64_t seed, int hk, Divisor gv,
-             Divisor span, uint32_t shards, unsigned long long* __restrict__ counts) {
+k_route_hist(const K* __restrict__ keys, const VT* __restrict__ vals, uint64_t n, uint64_t val_base,
+             Own own, uint32_t shards, unsigned long long* __restrict__ counts) {
     __shared__ uint32_t sh[256];
     for (uint32_t i = threadIdx.x; i < shards; i += blockDim.x) sh[i] = 0;
     __syncthreads();
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-        atomicAdd(sh + owner_of<POW2>(keys[i], seed, hk, gv, span), 1u);
+        atomicAdd(sh + own(uint64_t(keys[i]), vals ? uint64_t(vals[i]) : val_base + i), 1u);
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < shards; i += blockDim.x)
         if (sh[i]) atomicAdd(counts + i, (unsigned long long)sh[i]);
 }
 
-template <typename K, typename VT, int POW2>
+// REC: owner-grouped AoS records {key, value} (EntryT<K, VT>::T, the binned
+// build's entry type: one buffer, one all-to-all) instead of SoA keys / values.
+template <typename K, typename VT, typename Own, bool REC>
 __global__ void __launch_bounds__(kRouteBlock)
 k_route_scatter(const K* __restrict__ keys, const VT* __restrict__ vals, uint64_t n,
-                uint64_t val_base, uint64_t seed, int hk, Divisor gv, Divisor span,
-                uint32_t shards, unsigned long long* __restrict__ cursor, K* __restrict__ okeys,
-                VT* __restrict__ ovals) {
+                uint64_t val_base, Own own, uint32_t shards, unsigned long long* __restrict__ cursor,
+                K* __restrict__ okeys, VT* __restrict__ ovals,
+                typename EntryT<K, VT>::T* __restrict__ orec) {
     __shared__ K s_k[kRouteTile];
     __shared__ VT s_v[kRouteTile];
     __shared__ uint8_t s_o[kRouteTile];
@@ -65,24 +79,43 @@ k_route_scatter(const K* __restrict__ keys, const VT* __restrict__ vals, uint64_
         for (uint32_t d = tid; d < shards; d += kRouteBlock) s_cnt[d] = 0;
         __syncthreads();
         K kk[kRouteItems];
+        VT vv[kRouteItems];
         uint32_t orank[kRouteItems];
 #pragma unroll
         for (int k = 0; k < kRouteItems; ++k) {
             const uint32_t j = tid + k * kRouteBlock;
             if (j < cnt) {
                 kk[k] = keys[t0 + j];
-                const uint32_t o = owner_of<POW2>(kk[k], seed, hk, gv, span);
+                vv[k] = vals ? vals[t0 + j] : VT(val_base + t0 + j);
+                const uint32_t o = own(uint64_t(kk[k]), uint64_t(vv[k]));
                 orank[k] = (o << 16) | atomicAdd(s_cnt + o, 1u);
             }
         }
         __syncthreads();
-        if (tid == 0) {
-            uint32_t acc = 0;
-            for (uint32_t d = 0; d < shards; ++d) {
-                const uint32_t c = s_cnt[d];
-                s_off[d] = acc;
-                if (c) s_gbo[d] = atomicAdd(cursor + d, (unsigned long long)c) - acc;
-                acc += c;
+        if (tid < 32) {
+            // exclusive scan of <= 256 shard counts by one warp
+            uint32_t c[8], run = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t d = tid * 8 + q;
+                c[q] = d < shards ? s_cnt[d] : 0;
+                run += c[q];
+            }
+            uint32_t inc = run;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+                if (int(tid) >= d) inc += y;
+            }
+            uint32_t acc = inc - run;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t d = tid * 8 + q;
+                if (d < shards) {
+                    s_off[d] = acc;
+                    if (c[q]) s_gbo[d] = atomicAdd(cursor + d, (unsigned long long)c[q]) - acc;
+                }
+                acc += c[q];
             }
         }
         __syncthreads();
@@ -93,35 +126,37 @@ k_route_scatter(const K* __restrict__ keys, const VT* __restrict__ vals, uint64_
                 const uint32_t o = orank[k] >> 16;
                 const uint32_t slot = s_off[o] + (orank[k] & 0xFFFFu);
                 s_k[slot] = kk[k];
-                s_v[slot] = vals ? vals[t0 + j] : VT(val_base + t0 + j);
+                s_v[slot] = vv[k];
                 s_o[slot] = uint8_t(o);
             }
         }
         __syncthreads();
         for (uint32_t j = tid; j < cnt; j += kRouteBlock) {
             const uint64_t dst = s_gbo[s_o[j]] + j;
-            okeys[dst] = s_k[j];
-            ovals[dst] = s_v[j];
+            if constexpr (REC) {
+                orec[dst] = EntryT<K, VT>::make(s_k[j], s_v[j]);
+            } else {
+                okeys[dst] = s_k[j];
+                if (ovals) ovals[dst] = s_v[j];  // keys-only routing (count-only probes)
+            }
         }
         __syncthreads();
     }
 }
 
-template <typename K, typename VT, int POW2>
-static cudaError_t route_typed(const void* keys, const void* vals, uint64_t n, uint64_t val_base,
-                               uint64_t seed, int hk, uint64_t V, uint64_t vbase, uint64_t nloc,
-                               uint64_t span_v, uint32_t G, void* out_keys, void* out_vals,
-                               uint64_t* shard_counts, cudaStream_t s) {
-    const Divisor gv = make_divisor(V, vbase);  // (h mod V) - vbase
-    const Divisor span = make_divisor(span_v ? span_v : (nloc + G - 1) / G);
+template <typename K, typename VT, typename Own, bool REC>
+static cudaError_t route_impl(const void* keys, const void* vals, uint64_t n, uint64_t val_base,
+                              const Own& own, uint32_t G, void* out_keys, void* out_vals,
+                              void* out_rec, uint64_t* shard_counts, cudaStream_t s) {
     auto* counts = reinterpret_cast<unsigned long long*>(shard_counts);
     cudaError_t e = cudaMemsetAsync(counts, 0, G * 8, s);
     if (e != cudaSuccess || n == 0) return e;
     const int sms = num_sms();
     const unsigned gh = unsigned(std::min<uint64_t>((n + kRouteBlock - 1) / kRouteBlock, uint64_t(sms) * 4));
     HG_LAUNCH("k11_route_hist", s,
-              k_route_hist<K, POW2><<<gh, kRouteBlock, 0, s>>>(static_cast<const K*>(keys), n, seed,
-                                                               hk, gv, span, G, counts));
+              (k_route_hist<K, VT, Own><<<gh, kRouteBlock, 0, s>>>(
+                  static_cast<const K*>(keys), static_cast<const VT*>(vals), n, val_base, own, G,
+                  counts)));
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     // cursor[d] = exclusive prefix of counts
     unsigned long long* cursor = nullptr;
@@ -135,29 +170,44 @@ static cudaError_t route_typed(const void* keys, const void* vals, uint64_t n, u
         const uint64_t tiles = (n + kRouteTile - 1) / kRouteTile;
         const unsigned gs = unsigned(std::min<uint64_t>(tiles, uint64_t(sms) * 2));
         HG_LAUNCH("k11_route_scatter", s,
-                  (k_route_scatter<K, VT, POW2><<<gs, kRouteBlock, 0, s>>>(
-                      static_cast<const K*>(keys), static_cast<const VT*>(vals), n, val_base, seed,
-                      hk, gv, span, G, cursor, static_cast<K*>(out_keys),
-                      static_cast<VT*>(out_vals))));
+                  (k_route_scatter<K, VT, Own, REC><<<gs, kRouteBlock, 0, s>>>(
+                      static_cast<const K*>(keys), static_cast<const VT*>(vals), n, val_base, own, G,
+                      cursor, static_cast<K*>(out_keys), static_cast<VT*>(out_vals),
+                      static_cast<typename EntryT<K, VT>::T*>(out_rec))));
         e = cudaGetLastError();
     }
     cudaFreeAsync(cursor, s);
     return e;
 }
 
+template <typename K, typename VT>
+static cudaError_t route_hash_typed(const void* keys, const void* vals, uint64_t n, uint64_t val_base,
+                                    uint64_t seed, int hash_kind, uint64_t V, uint64_t vbase,
+                                    uint64_t nloc, uint64_t span, uint32_t G, void* out_keys,
+                                    void* out_vals, void* out_rec, uint64_t* shard_counts,
+                                    cudaStream_t s) {
+    const Divisor gv = make_divisor(V, vbase);  // (h mod V) - vbase
+    const Divisor sp = make_divisor(span ? span : (nloc + G - 1) / G);
+    return dispatch_hash_mode(hash_mode(V, hash_kind), [&](auto m) {
+        constexpr int HM = decltype(m)::value;
+        const OwnHash<HM> own{seed, gv, sp};
+        return out_rec ? route_impl<K, VT, OwnHash<HM>, true>(keys, vals, n, val_base, own, G, nullptr,
+                                                             nullptr, out_rec, shard_counts, s)
+                       : route_impl<K, VT, OwnHash<HM>, false>(keys, vals, n, val_base, own, G,
+                                                              out_keys, out_vals, nullptr,
+                                                              shard_counts, s);
+    });
+}
+
 cudaError_t route_keys(const void* keys, int key_bytes, const void* vals, int val_bytes,
                        uint64_t n, uint64_t val_base, uint64_t seed, int hash_kind,
                        uint64_t global_vertices, uint64_t vertex_base, uint64_t local_vertices,
                        uint64_t span, uint32_t shards, void* out_keys, void* out_vals,
-                       uint64_t* shard_counts, cudaStream_t s) {
-    const int hm = hash_mode(global_vertices, hash_kind);
-#define HG_ROUTE(K, VT)                                                                        \
-    return dispatch_hash_mode(hm, [&](auto m) {                                                \
-        return route_typed<K, VT, decltype(m)::value>(keys, vals, n, val_base, seed, hash_kind, \
-                                                      global_vertices, vertex_base,            \
-                                                      local_vertices, span, shards, out_keys,  \
-                                                      out_vals, shard_counts, s);              \
-    })
+                       uint64_t* shard_counts, cudaStream_t s, void* out_records) {
+#define HG_ROUTE(K, VT)                                                                          \
+    return route_hash_typed<K, VT>(keys, vals, n, val_base, seed, hash_kind, global_vertices,     \
+                                   vertex_base, local_vertices, span, shards, out_keys, out_vals, \
+                                   out_records, shard_counts, s)
     if (key_bytes == 4) {
         if (val_bytes == 4) HG_ROUTE(uint32_t, uint32_t);
         HG_ROUTE(uint32_t, uint64_t);
@@ -165,6 +215,17 @@ cudaError_t route_keys(const void* keys, int key_bytes, const void* vals, int va
     if (val_bytes == 4) HG_ROUTE(uint64_t, uint32_t);
     HG_ROUTE(uint64_t, uint64_t);
 #undef HG_ROUTE
+}
+
+cudaError_t route_pairs(const void* left, const void* right, int pair_bytes, uint64_t n,
+                        uint64_t span, uint32_t shards, void* out_records, uint64_t* shard_counts,
+                        cudaStream_t s) {
+    const OwnVal own{make_divisor(span)};
+    if (pair_bytes == 4)
+        return route_impl<uint32_t, uint32_t, OwnVal, true>(left, right, n, 0, own, shards, nullptr,
+                                                           nullptr, out_records, shard_counts, s);
+    return route_impl<uint64_t, uint64_t, OwnVal, true>(left, right, n, 0, own, shards, nullptr,
+                                                       nullptr, out_records, shard_counts, s);
 }
 
 }  // namespace hg

@@ -5,15 +5,20 @@ bin = v / ceil(V / bins)) at bins = G picks the owner GPU of vertex v, so the
 global table is the concatenation of G local tables over contiguous vertex
 ranges. Per rank:
 
-  build   route   keys -> owner-grouped (key, global index) send buffers
-                  (K11, hg_route; one pass of the partition machinery)
-          counts  all_gather of the G x G send-count matrix
-          all2all torch.distributed all_to_all_single over NCCL / NVLink
-          build   local V1/V2 build over [base, base + S) with the global hash
-                  (hg_build with global_vertices / vertex_base)
-  probe   route probes the same way (value = global probe position), local
-          probe_standard, all_reduce of (match_count, key_comparisons);
-          pairs stay on the owner (or are gathered for parity checks).
+  build   route   keys -> owner-grouped AoS records {key, global index} in
+                  one buffer (K11, hg_route_records)
+          counts  all_to_all_single of the G send counts (device), one D2H
+                  of (send, recv) counts -- NCCL needs host-known split sizes
+          all2all ONE all_to_all_single of the records over NCCL / NVLink
+          build   local V1/V2 build over [base, base + S) with the global hash,
+                  straight from the received records (hg_build_records: the
+                  binned build's first pass reads them, no unpack)
+  probe   count-only: route probe keys (hg_route), one all_to_all of the keys,
+          local probe_standard, all_reduce of (match_count, key_comparisons);
+          pairs: route probes as records {key, global probe position}, local
+          probe with pairs, then the REVERSE route (hg_route_pairs, owner =
+          probe position / probes per rank) and all_to_all return every pair
+          to the rank that holds its probe.
 
 The result equals the reference's single table: offsets of shard g are its
 local offsets + the number of entries on shards < g, and per-vertex entry
@@ -75,8 +80,82 @@ class CudaEngine:
         from .hashgraph import IdentityHasher
         fn = build_v2 if self.variant == 2 else build_v1
         hasher = IdentityHasher() if hash_kind == 1 else None
+        if count == 0:  # this rank owns no vertex (V < G): an empty unsharded table
+            return fn(keys, cfg, vertex_count=1, hasher=hasher, vals=vals)
         return fn(keys, cfg, vertex_count=count, hasher=hasher, vals=vals,
                   shard=(global_vertices, base))
+
+    @staticmethod
+    def record_words(key_width: int, val_width: int) -> int:
+        """int64 words per AoS record (8-byte records for 4 + 4, else 16)."""
+        return 1 if key_width == 4 and val_width == 4 else 2
+
+    def route_records(self, keys, val_width: int, val_base: int, seed: int, hash_kind: int,
+                      global_vertices: int, shards: int):
+        """Owner-grouped AoS records {key, global index} (hg_route_records) as an
+        int64 tensor of n * record_words elements, plus device counts."""
+        t = self.torch
+        ka = _Arr(keys)
+        w = self.record_words(ka.width, val_width)
+        out = t.empty(max(ka.n, 1) * w, dtype=t.int64, device="cuda")
+        counts = t.zeros(shards, dtype=t.int64, device="cuda")
+        s = t.cuda.current_stream().cuda_stream
+        _check(_lib.lib().hg_route_records(ka.ptr, ka.width, None, val_width, ka.n, val_base,
+                                           seed, hash_kind, global_vertices, shards,
+                                           out.data_ptr(), counts.data_ptr(), s))
+        return out[: ka.n * w], counts
+
+    def build_records(self, records, key_width: int, val_width: int, global_vertices: int,
+                      base: int, count: int, cfg: BuildConfig, hash_kind: int) -> HashGraph:
+        """Local build straight from received records (hg_build_records)."""
+        from .hashgraph import BUILD_BINNED, BUILD_SIMPLE, ExecMode
+        t = self.torch
+        w = self.record_words(key_width, val_width)
+        n = records.numel() // w
+        c = _lib.hg_build_config()
+        _lib.lib().hg_build_config_init(C.byref(c))
+        c.load_factor = float(cfg.load_factor)
+        c.hash_seed = int(cfg.hash_seed)
+        c.variant = BUILD_BINNED if self.variant == 2 else BUILD_SIMPLE
+        c.hash_kind = int(hash_kind)
+        c.stable = 1 if cfg.mode == ExecMode.sequential else 0
+        c.partition_vertices = int(cfg.partition_vertices)
+        if count:
+            c.vertex_count = int(count)
+            c.global_vertices, c.vertex_base = int(global_vertices), int(base)
+        else:  # this rank owns no vertex: an empty unsharded table
+            c.vertex_count = 1
+        s = t.cuda.current_stream().cuda_stream
+        h = C.c_void_p()
+        _check(_lib.lib().hg_build_records(records.data_ptr() if n else None, key_width,
+                                           val_width, n, C.byref(c), s, C.byref(h)))
+        return HashGraph(h.value, s)
+
+    def unpack_records(self, records, key_width: int, val_width: int):
+        """(keys, values) views of received records, contiguous for the C-ABI."""
+        t = self.torch
+        if self.record_words(key_width, val_width) == 1:
+            kv = records.view(t.int32).view(-1, 2)
+            return kv[:, 0].contiguous(), kv[:, 1].contiguous()
+        kv = records.view(-1, 2)
+        keys = kv[:, 0].contiguous()
+        if key_width == 4:
+            keys = keys.to(t.int32)
+        vals = kv[:, 1].contiguous()
+        return keys, (vals.to(t.int32) if val_width == 4 else vals)
+
+    def route_pairs(self, left, right, span: int, shards: int):
+        """Pairs grouped by the rank holding their probe (owner = right / span),
+        AoS records {left, right} (hg_route_pairs) + device counts."""
+        t = self.torch
+        la, ra = _Arr(left), _Arr(right)
+        n = la.n
+        out = t.empty(max(n, 1) * 2, dtype=left.dtype, device="cuda")
+        counts = t.zeros(shards, dtype=t.int64, device="cuda")
+        s = t.cuda.current_stream().cuda_stream
+        _check(_lib.lib().hg_route_pairs(la.ptr, ra.ptr, la.width, n, span, shards,
+                                         out.data_ptr(), counts.data_ptr(), s))
+        return out[: 2 * n], counts
 
     def probe_totals(self, table: HashGraph, probes):
         t = self.torch
@@ -88,9 +167,8 @@ class CudaEngine:
         """Pairs (build global index, probe global index) as two tensors."""
         t = self.torch
         n = probes.numel()
-        counts = t.zeros(n, dtype=t.int32, device="cuda")
         res = t.zeros(2, dtype=t.int64, device="cuda")
-        probe_device(table, probes, res, counts=counts)
+        probe_device(table, probes, res)  # count-only pass sizes the pair buffer
         total = int(res[0].item())
         pw = 8 if table.val_width == 8 or n > (1 << 32) else 4
         pairs = t.empty(max(total, 1) * 2, dtype=t.int32 if pw == 4 else t.int64, device="cuda")
@@ -126,24 +204,46 @@ class ShardedHashGraph:
         self.table: Optional[ShardedTable] = None
         self.last_local_n = self.last_local_m = self.last_local_c = 0
         self.local_vertices = 0
+        self.last_build_bytes = self.last_probe_bytes = 0
+        self.exchange_events = None  # a list -> time every all_to_all (bench)
 
     # -------------------------------------------------------------- plumbing
-    def _exchange(self, send_k, send_v, counts):
-        """All-to-all of owner-grouped SoA buffers; returns received (k, v)."""
+    def _count_matrix(self, counts):
+        """G x G send-count matrix M[g][p] (rank g -> rank p) from every rank's
+        device counts: one all_gather, one D2H (NCCL's all-to-all takes host
+        split sizes, and the local build sizes its scratch from its count)."""
         import torch
-        dist = self.dist
         G = self.world
         cnt = counts.to(torch.int64)
         gathered = [torch.zeros_like(cnt) for _ in range(G)]
-        dist.all_gather(gathered, cnt, group=self.group)
-        send_splits = [int(x) for x in cnt.cpu().tolist()]
-        recv_splits = [int(g[self.rank].item()) for g in gathered]
-        nrecv = sum(recv_splits)
-        recv_k = send_k.new_empty(nrecv)
-        recv_v = send_v.new_empty(nrecv)
-        dist.all_to_all_single(recv_k, send_k, recv_splits, send_splits, group=self.group)
-        dist.all_to_all_single(recv_v, send_v, recv_splits, send_splits, group=self.group)
-        return recv_k, recv_v
+        self.dist.all_gather(gathered, cnt, group=self.group)
+        flat = torch.stack(gathered).cpu().tolist()
+        return [[int(x) for x in row] for row in flat]
+
+    def _alltoall(self, send, M, words: int = 1):
+        """ONE all_to_all_single of an owner-grouped buffer (`words` elements
+        per item) by the count matrix M; returns the received buffer."""
+        r = self.rank
+        send_splits = [c * words for c in M[r]]
+        recv_splits = [M[g][r] * words for g in range(self.world)]
+        recv = send.new_empty(sum(recv_splits))
+        ev = None
+        if self.exchange_events is not None and send.is_cuda:
+            import torch
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
+        self.dist.all_to_all_single(recv, send, recv_splits, send_splits, group=self.group)
+        if ev is not None:
+            ev[1].record()
+            self.exchange_events.append(ev)
+        return recv
+
+    def exchange_ms(self) -> float:
+        """Device time of the all-to-alls recorded since exchange_events was
+        set to [] (CUDA events on the current stream around each exchange)."""
+        ms = sum(a.elapsed_time(b) for a, b in self.exchange_events or [])
+        self.exchange_events = None
+        return ms
 
     def _allreduce_sum(self, x):
         self.dist.all_reduce(x, group=self.group)
@@ -155,50 +255,75 @@ class ShardedHashGraph:
               partition_vertices: int = 0) -> ShardedTable:
         """keys: this rank's slice of the global input, whose first element is
         global position `global_offset`; global_n = total keys on all ranks."""
-        import torch
         V = vertex_count or derived_vertex_count(global_n, load_factor)
         base, count = shard_range(V, self.world, self.rank)
-        val_width = 4 if global_n <= (1 << 32) else 8
-        send_k, send_v, counts = self.engine.route(keys, None, val_width, global_offset,
-                                                   self.hash_seed, self.hash_kind, V, self.world)
-        recv_k, recv_v = self._exchange(send_k, send_v, counts)
+        kw = keys.element_size()
+        vw = 4 if global_n <= (1 << 32) else 8
+        w = self.engine.record_words(kw, vw)
+        rec, counts = self.engine.route_records(keys, vw, global_offset, self.hash_seed,
+                                                self.hash_kind, V, self.world)
+        M = self._count_matrix(counts)
+        recv = self._alltoall(rec, M, w)
         cfg = BuildConfig(load_factor=load_factor, hash_seed=self.hash_seed, mode=mode,
                           partition_vertices=partition_vertices)
-        table = self.engine.build(recv_k, recv_v, V, base, max(count, 1), cfg, self.hash_kind)
-        n_local = torch.tensor([recv_k.numel()], dtype=torch.int64, device=recv_k.device)
-        all_n = [torch.zeros_like(n_local) for _ in range(self.world)]
-        self.dist.all_gather(all_n, n_local, group=self.group)
-        edge_base = sum(int(x.item()) for x in all_n[: self.rank])
-        self.table = ShardedTable(table, V, base, count, edge_base, int(recv_k.numel()))
-        self.last_local_n = int(recv_k.numel())
+        table = self.engine.build_records(recv, kw, vw, V, base, count, cfg, self.hash_kind)
+        n_of = [sum(M[g][p] for g in range(self.world)) for p in range(self.world)]
+        edge_base = sum(n_of[: self.rank])
+        local_n = n_of[self.rank]
+        self.table = ShardedTable(table, V, base, count, edge_base, local_n)
+        self.last_local_n = local_n
         self.local_vertices = count
+        self.last_build_bytes = self._nvlink_bytes(M, w * 8)
         return self.table
+
+    def _nvlink_bytes(self, M, item_bytes: int) -> int:
+        """Bytes this rank sends to OTHER ranks (its NVLink egress) in one
+        exchange with count matrix M."""
+        r = self.rank
+        return sum(c for p, c in enumerate(M[r]) if p != r) * item_bytes
 
     # -------------------------------------------------------------- probe
     def probe_count(self, probes, global_offset: int = 0):
         """probe_standard match_count / key_comparisons over all ranks'
-        probes (device tensor [2] after the all_reduce)."""
+        probes (device tensor [2] after the all_reduce). Only the probe keys
+        travel (count-only needs no positions)."""
         st = self.table
-        width = 4 if probes.element_size() == 4 else 8
-        send_k, send_v, counts = self.engine.route(probes, None, 4, global_offset, self.hash_seed,
-                                                   self.hash_kind, st.global_vertices, self.world)
-        recv_k, _ = self._exchange(send_k, send_v, counts)
+        send_k, _, counts = self.engine.route(probes, None, 4, global_offset, self.hash_seed,
+                                              self.hash_kind, st.global_vertices, self.world)
+        M = self._count_matrix(counts)
+        recv_k = self._alltoall(send_k, M)
         self.last_local_m = int(recv_k.numel())
+        self.last_probe_bytes = self._nvlink_bytes(M, probes.element_size())
         tot = self.engine.probe_totals(st.table, recv_k)
-        self.last_local_c = int(tot[1].item()) if self.world > 0 else 0
+        self.last_local_c = int(tot[1].item())
         return self._allreduce_sum(tot)
 
     def probe_pairs(self, probes, global_offset: int, global_m: int):
-        """Match pairs (build global index, probe global index) owned by this
-        rank, plus the all-reduced (match_count, key_comparisons)."""
+        """probe_standard with pairs: returns, on the rank that holds the
+        probes, the pairs (build global index, probe global index) of ITS
+        probes -- routed to the table owner as records {key, global probe
+        position}, probed there, and routed back by probe position
+        (hg_route_pairs) -- plus the all-reduced (match_count,
+        key_comparisons). Ranks hold equal probe slices: rank r's probes have
+        global positions [r * m, (r + 1) * m)."""
         st = self.table
+        m = probes.numel()
+        if global_offset != self.rank * m:
+            raise ValueError("probe_pairs expects equal probe slices (global_offset = rank * m)")
+        kw = probes.element_size()
         pw = 4 if global_m <= (1 << 32) else 8
-        send_k, send_v, counts = self.engine.route(probes, None, pw, global_offset,
-                                                   self.hash_seed, self.hash_kind,
-                                                   st.global_vertices, self.world)
-        recv_k, recv_v = self._exchange(send_k, send_v, counts)
-        left, right, tot = self.engine.probe_pairs(st.table, recv_k, recv_v)
-        return left, right, self._allreduce_sum(tot)
+        w = self.engine.record_words(kw, pw)
+        rec, counts = self.engine.route_records(probes, pw, global_offset, self.hash_seed,
+                                                self.hash_kind, st.global_vertices, self.world)
+        M = self._count_matrix(counts)
+        recv = self._alltoall(rec, M, w)
+        keys, pos = self.engine.unpack_records(recv, kw, pw)
+        left, right, tot = self.engine.probe_pairs(st.table, keys, pos)
+        # reverse route: every pair back to the rank holding its probe
+        prec, pcounts = self.engine.route_pairs(left, right, max(m, 1), self.world)
+        M2 = self._count_matrix(pcounts)
+        back = self._alltoall(prec, M2, 2).view(-1, 2)
+        return back[:, 0], back[:, 1], self._allreduce_sum(tot)
 
     # -------------------------------------------------------------- step
     def build_and_probe(self, keys, probes, result, n_per_rank: Optional[int] = None):

@@ -223,8 +223,9 @@ def test_partial_last_partition(oracle, cuda, tail):
 
 def test_sharded_engine_over_nccl_world1(cuda, oracle):
     """The N > 1 bench path end to end on one GPU: ShardedHashGraph over a
-    world-1 NCCL group (hg_route, count all_gather, all_to_all_single, shard
-    build with vertex_base, routed probe, all_reduce) equals the unsharded
+    world-1 NCCL group (hg_route_records, count all_gather, one
+    all_to_all_single, hg_build_records with vertex_base, routed probe,
+    all_reduce; pairs routed back by probe position) equals the unsharded
     build and probe; export_global rebases offsets like the reference."""
     import socket
     import torch.distributed as dist
@@ -248,6 +249,22 @@ def test_sharded_engine_over_nccl_world1(cuda, oracle):
         tot = eng.probe_count(probes, 0)
         ref = hg.probe_standard(hg.build_v2(keys), probes)
         assert tuple(int(x) for x in tot.cpu().tolist()) == (ref.match_count, ref.key_comparisons)
+        # pairs: routed as records {key, position}, probed, routed back by
+        # probe position (hg_route_pairs) -- equal to the unsharded pair set
+        mix = cuda.cat([keys[: n // 4], probes[: n // 4]])
+        left, right, ptot = eng.probe_pairs(mix, 0, mix.numel())
+        rp = hg.probe_standard(hg.build_v2(keys), mix,
+                               hg.ProbeOptions(materialize=True, pair_cap=1 << 24))
+        assert tuple(int(x) for x in ptot.cpu().tolist()) == (rp.match_count, rp.key_comparisons)
+        got = np.stack([left.cpu().numpy(), right.cpu().numpy()], 1).astype(np.uint64)
+        exp = np.stack([rp.pairs["left_index"], rp.pairs["right_index"]], 1).astype(np.uint64)
+        assert len(got) == rp.match_count
+        assert (got[np.lexsort((got[:, 1], got[:, 0]))] == exp[np.lexsort((exp[:, 1], exp[:, 0]))]).all()
+        # records in, table out: hg_route_records + hg_build_records (V1 too)
+        eng1 = sharded.ShardedHashGraph(1, 0, variant=1)
+        eng1.build(keys, 0, n)
+        off1, _, _ = eng1.export_global()
+        assert (off1 == o.offsets).all()
         res = cuda.zeros(2, dtype=cuda.int64, device="cuda")
         eng.build_and_probe(keys, probes, res)
         assert int(res[0]) == ref.match_count

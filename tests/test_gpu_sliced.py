@@ -107,17 +107,28 @@ def test_v2_two_pow_31_keys_full_size(cuda):
     """a 2^31-key V2 build on one GPU (V = 2^31, 8 slices of
     2^28 vertices), validated on the device with its input keys (offsets
     monotone, offsets[V] = N, hash consistency, key == input[index],
-    permutation), and a probe of the first 2^24 keys finds each at least once."""
+    permutation); the sliced probe of 2^24 probes (half of them build keys)
+    equals the direct-gather probe."""
     n = 1 << 31
     keys = cuda.empty(n, dtype=cuda.int32, device="cuda")
     hg.generate(keys, kind=0, seed=1)
     t = hg.build_v2(keys)
     assert t.num_vertices() == n and t.num_edges() == n
     assert hg.validate_csr(t, n, keys) is None
-    counts = cuda.zeros(1 << 24, dtype=cuda.int32, device="cuda")
-    res = cuda.zeros(2, dtype=cuda.int64, device="cuda")
-    hg.probe_device(t, keys[: 1 << 24], res, counts=counts)
-    assert bool((counts >= 1).all())
+    m = 1 << 24
+    probes = cuda.cat([keys[: m // 2], keys[-m // 2:] ^ 0x5A5A5A5A])
+    # auto = the sliced probe (V = 2^31 is too wide for one partitioned pass):
+    # probes routed into 2^28-vertex slices, each probed partitioned; against
+    # the direct-gather probe (method 1), totals and per-probe counts
+    res, res1 = (cuda.zeros(2, dtype=cuda.int64, device="cuda") for _ in range(2))
+    counts, counts1 = (cuda.zeros(m, dtype=cuda.int32, device="cuda") for _ in range(2))
+    hg.probe_device(t, probes, res, counts=counts)
+    hg.probe_device(t, probes, res1, counts=counts1, method=1)
+    assert res.tolist() == res1.tolist()
+    assert bool((counts == counts1).all()) and bool((counts[: m // 2] >= 1).all())
+    res.zero_()
+    hg.probe_device(t, probes, res)  # count-only: slices get keys only
+    assert res.tolist() == res1.tolist()
     t.close()
 
 
