@@ -307,6 +307,10 @@ def run_reference(args):
 
 # ------------------------------------------------------------------ secondary configs
 
+def log(msg: str) -> None:
+    print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def _timed(torch, stream, fn, reps=3):
     """Average ms of fn() over reps (after one untimed call), CUDA events on `stream`."""
     fn()
@@ -323,19 +327,24 @@ def _timed(torch, stream, fn, reps=3):
 def bench_c3(torch, hg, stream, sp, peak, rows, log2n=28):
     """C3: 2^28 u64 keys ~ Zipf(s = 1.0) over 2^24 ranks with u64 values,
     binned and simple builds across the load sweep (G keys/s = N / t), and
-    probe_standard (count) of 2^28 probes drawn from the same Zipf
-    distribution (seed 2: heavy ranks hit long segments) into each V2 table
-    (G probes/s = M / t). Rooflines from SURVEY.md 8(d) bytes with the exact C."""
+    probe_standard (count) of 2^28 probes of uniformly drawn ranks (seed 2)
+    into each V2 table (G probes/s = M / t): every rank is probed equally, so
+    the heavy ranks' long segments are walked (by the warp) about M / 2^24
+    times each. (Zipf-distributed probes would make the join itself explode:
+    the top rank holds ~6 % of both sides, ~2^48 comparisons.) Rooflines from
+    SURVEY.md 8(d) bytes with the exact C."""
     n = 1 << log2n
     cdf = torch.tensor(hg.zipf_cdf(1 << 24, 1.0), dtype=torch.float64, device="cuda")
     keys = torch.empty(n, dtype=torch.int64, device="cuda")
     hg.generate(keys, kind=3, seed=1, ref=cdf)
     probes = torch.empty(n, dtype=torch.int64, device="cuda")
-    hg.generate(probes, kind=3, seed=2, ref=cdf)
+    ucdf = torch.arange(1, (1 << 24) + 1, dtype=torch.float64, device="cuda") / float(1 << 24)
+    hg.generate(probes, kind=3, seed=2, ref=ucdf)  # uniform ranks through the same key map
+    del ucdf
     vals = torch.arange(n, dtype=torch.int64, device="cuda")
     res = torch.zeros(2, dtype=torch.int64, device="cuda")
     out = {"workload": "2^28 u64 Zipf(1.0) keys over 2^24 ranks, u64 values = position; "
-                       "2^28 Zipf(1.0) probes (seed 2)"}
+                       "2^28 probes of uniform ranks (seed 2)"}
     for load in (0.5, 1.0, 1.5, 2.0, 4.0):
         row = {}
         nv = hg.derived_vertex_count(n, load)
@@ -657,13 +666,18 @@ def run_b200(args):
             "matches_equal_probe_standard": pn_matches == matches}
         rows.append(csv_row("probe", "probe_new", n + m, 1.0, ti / reps, n + m,
                             matches=pn_matches, alg=extras["probe_new"]["intersect_roofline"]))
+        log("c3")
         extras["c3_zipf"] = bench_c3(torch, hg, stream, sp, peak, rows)
+        log("c4")
         extras["c4_join"] = bench_c4(torch, hg, stream, sp, peak, rows)
+        log("multiplicity")
         extras["multiplicity"] = bench_multiplicity(torch, hg, stream, sp, peak, rows)
+        log("phases done")
         line["phases"] = extras
 
     # ---- e2e through the public API with pinned HOST buffers
     if not args.no_e2e and world == 1:
+        log("e2e")
         hkeys = keys.cpu().pin_memory()
         hprobes = probes.cpu().pin_memory()
         torch.cuda.synchronize()
@@ -726,6 +740,7 @@ def run_b200(args):
                                "hg_route / hg_build / hg_probe, NCCL all_to_all) -> totals"}
 
     if not args.no_cpu and world == 1 and rank == 0:
+        log("cpu baseline")
         # the reference on the host cores: the same 2^28 config, all threads,
         # two trials (~30 s of CPU work), plus a 1-thread row on a 2^22 sample
         try:
