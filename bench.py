@@ -513,15 +513,21 @@ def run_b200(args):
         torch.cuda.synchronize()
 
     # ---- timed region (device-resident inputs; each input 1 GiB > 126 MB L2)
-    _lib.profiler_enable(True)
+    dbg = os.environ.get("BENCH_DEBUG", "")
+    _lib.profiler_enable("noprof" not in dbg)
     _lib.profiler_collect()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local if "noclock" not in dbg else 10 ** 6)
     barrier()
     with clocks:
         ev0.record(stream)
         for _ in range(args.steps):
+            h0 = time.perf_counter()
             step()
+            if "sync" in dbg:
+                torch.cuda.synchronize()
+            if dbg:
+                log(f"step host {1e3 * (time.perf_counter() - h0):.1f} ms")
         ev1.record(stream)
         barrier()
     _lib.profiler_enable(False)
@@ -562,8 +568,11 @@ def run_b200(args):
     dom = max((k for k in kern if alg_bytes(k, 1, 1, 1, 1) > 0), key=lambda k: kern[k][1])
     dl, dms = kern[dom]
     avg_ms = dms / dl
-    ab = alg_bytes(dom, local_n, local_v, local_m, comparisons if world == 1 else
-                   int(engine.last_local_c))
+    # alg_bytes() is the kernel's traffic for the whole step (summed over its
+    # launches when a sliced table launches it once per vertex-range slice)
+    ab_step = alg_bytes(dom, local_n, local_v, local_m, comparisons if world == 1 else
+                        int(engine.last_local_c))
+    ab = ab_step * args.steps // dl  # per launch
     achieved = ab / (avg_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -573,8 +582,8 @@ def run_b200(args):
                 "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                 "alg_bytes_per_launch": ab, "avg_launch_ms": round(avg_ms, 4),
                 "peak_source": peak_src,
-                "step_alg_bytes": sum(alg_bytes(k, local_n, local_v, local_m, comparisons) * kern[k][0]
-                                      for k in kern) // max(1, args.steps)}
+                "step_alg_bytes": sum(alg_bytes(k, local_n, local_v, local_m, comparisons)
+                                      for k in kern)}
     ref_bytes = reference_alg_bytes(args.variant, local_n, local_v, local_m,
                                     comparisons if world == 1 else int(engine.last_local_c))
     roofline["step_alg_frac"] = round(roofline["step_alg_bytes"] / (ms * 1e-3) / 1e9 / peak, 4)

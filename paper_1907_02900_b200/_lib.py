@@ -11,7 +11,8 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhg_b200.so")
+# HG_B200_LIB: an alternate build of the same C-ABI (A/B tuning runs only)
+LIB_PATH = os.environ.get("HG_B200_LIB") or os.path.join(HERE, "libhg_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "hg_b200.h")
 
 HG_OK, HG_EINVAL, HG_ERANGE, HG_EOVERFLOW, HG_ENOMEM, HG_ECUDA, HG_ENCCL, HG_EUNSUPPORTED, HG_EIO = range(9)

@@ -37,6 +37,22 @@ int num_sms() {
     return sms;
 }
 
+// A table (or scratch) of more than 1/8 of device memory: the stream is
+// drained first, so that the pool serves it from the blocks freed by earlier
+// work on the stream (e.g. the previous table of a build / probe loop)
+// instead of growing while those frees are still pending -- near the memory
+// limit that growth stalls for hundreds of ms (measured at C5, 2^32 keys on
+// one GPU: 1.2 s steps instead of 207 ms).
+bool huge_allocation(uint64_t bytes) {
+    static uint64_t total = 0;
+    if (!total) {
+        size_t f = 0, t = 0;
+        cudaMemGetInfo(&f, &t);
+        total = t ? t : (uint64_t(180) << 30);
+    }
+    return bytes > total / 8;
+}
+
 size_t smem_optin() {
     static int bytes = 0;
     if (!bytes) {
@@ -293,6 +309,20 @@ static cudaError_t build_v1_impl(const TableDesc& t, const BuildArgs& a, cudaStr
 template <typename K, typename VT, typename OffT, int POW2>
 cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s);
 
+static const char* const kSliceNames[3] = {"slice_hist", "slice_split", "slice_split2"};
+
+// Geometry of the one-digit split into G vertex-range slices of 2^sshift
+// vertices: "partition" = slice.
+inline PartGeom slice_geom(uint32_t sshift, uint64_t G) {
+    PartGeom g;
+    g.pshift = sshift;
+    g.nparts = G;
+    g.bits = ceil_log2(G);
+    g.b1 = g.bits;
+    g.b2 = 0;
+    return g;
+}
+
 // Width (log2 vertices) of the slices a binned build is split into, 0 when
 // the whole vertex range fits 2^16 partitions of the tuned width (~4096
 // entries, 2048 for 16-byte entries; make_geom in hg_radix.cuh).
@@ -313,13 +343,13 @@ static uint32_t v2_slice_shift(const TableDesc& t, const BuildArgs& a, size_t en
 // Binned build over a vertex range wider than 2^16 partitions of the tuned
 // width (V > 2^28 at load 1, e.g. 2^31 keys or C5's 2^31-vertex shards). The
 // reference's bin split (core.hpp:192-197) is applied once more on top: K11
-// routes the keys into G slices of 2^sshift consecutive vertices as AoS
-// records {key, input position} (hg_shard.cu), then each slice is built by
-// the binned build (whose first pass reads the records) into its range of
-// the one table -- offsets written with the slice's entry
+// splits the keys into G slices of 2^sshift consecutive vertices as AoS
+// records {key, input position} (one pass of the partition machinery,
+// hg_radix.cuh), then each slice is built by the binned build (whose first
+// pass reads the records) into its range of the one table -- offsets written with the slice's entry
 // base (TableDesc::obase), keys / values at the slice's entry range -- so
 // every slice keeps the tuned partition geometry (two 8-bit digits, K7 at two
-// CTAs per SM). Extra traffic: one routing pass, N (kb + vb) read + written.
+// CTAs per SM). Extra traffic: one histogram + one split pass over the keys.
 template <typename K, typename VT, typename OffT, int HM>
 static cudaError_t build_v2_sliced(const TableDesc& t, const BuildArgs& a, uint32_t sshift,
                                    cudaStream_t s) {
@@ -327,23 +357,32 @@ static cudaError_t build_v2_sliced(const TableDesc& t, const BuildArgs& a, uint3
     const uint64_t G = (t.nv + S - 1) / S;
     if (G > 256) return cudaErrorInvalidValue;
     using E = typename EntryT<K, VT>::T;
+    // one multisplit pass with digit = local vertex >> sshift (hg_radix.cuh:
+    // histogram, scan, TMA-staged split) -> records grouped by slice
+    const PartGeom sg = slice_geom(sshift, G);
     const size_t rbytes = (t.n * sizeof(E) + 255) & ~size_t(255);
+    const size_t sbytes = ((G + 1) * 8 + 255) & ~size_t(255);
+    const size_t pbytes = PartitionScratch<K, VT, uint64_t>::bytes(sg, t.n);
     char* scratch = nullptr;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), rbytes + 256 * 8, s);
+    cudaError_t e = cudaSuccess;
+    if (huge_allocation(rbytes + sbytes + pbytes)) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), rbytes + sbytes + pbytes, s);
     if (e != cudaSuccess) return e;
     E* rec = reinterpret_cast<E*>(scratch);
-    uint64_t* dcnt = reinterpret_cast<uint64_t*>(scratch + rbytes);
-    uint64_t cnt[256];
+    uint64_t* dstart = reinterpret_cast<uint64_t*>(scratch + rbytes);
+    uint64_t cnt[257];
     do {
-        // slices as AoS records {key, input position}: each slice's binned
-        // build reads them directly in its first pass
-        if ((e = route_keys(a.keys, sizeof(K), a.vals, sizeof(VT), t.n, 0, t.seed, t.hash_kind,
-                            global_nv(t), t.vbase, t.nv, S, uint32_t(G), nullptr, nullptr, dcnt, s,
-                            rec)) != cudaSuccess)
+        const Divisor nv = make_divisor(global_nv(t), t.vbase);
+        if ((e = partition<K, VT, uint64_t, HM>(static_cast<const K*>(a.keys),
+                                                static_cast<const VT*>(a.vals), t.n, t.seed,
+                                                t.hash_kind, nv, sg, dstart, scratch + rbytes + sbytes,
+                                                rec, s, kSliceNames,
+                                                static_cast<const E*>(a.records))) != cudaSuccess)
             break;
-        if ((e = cudaMemcpyAsync(cnt, dcnt, G * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        if ((e = cudaMemcpyAsync(cnt, dstart, (G + 1) * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
             (e = cudaStreamSynchronize(s)) != cudaSuccess)
             break;
+        for (uint64_t g = 0; g < G; ++g) cnt[g] = cnt[g + 1] - cnt[g];  // slice sizes
         uint64_t start = 0;
         for (uint64_t g = 0; g < G && e == cudaSuccess; ++g) {
             TableDesc sub = t;
@@ -369,8 +408,8 @@ static cudaError_t build_v2_sliced(const TableDesc& t, const BuildArgs& a, uint3
     return e;
 }
 
-// AoS records -> SoA keys / values (the simple build and the sliced binned
-// build take SoA input; the binned build's first pass reads records directly).
+// AoS records -> SoA keys / values (the simple build takes SoA input; the
+// binned build's first pass, sliced or not, reads records directly).
 template <typename K, typename VT>
 __global__ void k_unpack_records(const typename EntryT<K, VT>::T* __restrict__ rec, uint64_t n,
                                  K* __restrict__ keys, VT* __restrict__ vals) {
@@ -411,8 +450,7 @@ static cudaError_t build_from_records_soa(const TableDesc& t, const BuildArgs& a
 template <typename K, typename VT, typename OffT>
 static cudaError_t build_typed(const TableDesc& t, const BuildArgs& a, cudaStream_t s) {
     const uint32_t sshift = a.variant == 2 ? v2_slice_shift(t, a, sizeof(typename EntryT<K, VT>::T)) : 0;
-    if (a.records && t.n && (a.variant != 2 || sshift))
-        return build_from_records_soa<K, VT, OffT>(t, a, s);
+    if (a.records && t.n && a.variant != 2) return build_from_records_soa<K, VT, OffT>(t, a, s);
     cudaError_t e = dispatch_hash_mode(hash_mode(global_nv(t), t.hash_kind), [&](auto hm) {
         constexpr int HM = decltype(hm)::value;
         if (sshift) return build_v2_sliced<K, VT, OffT, HM>(t, a, sshift, s);

@@ -261,7 +261,10 @@ static hg_status build_common(const void* keys, int32_t key_width, const void* v
     d.off_bytes = (n < (uint64_t(1) << 32) && nv <= (uint64_t(1) << 32)) ? 4 : 8;
     // offs is padded so that offs + 1 (the counter / cursor view) is 16-byte aligned.
     const uint64_t pad = 16 / d.off_bytes - 1;
-    cudaError_t e = cudaMallocAsync(&t->alloc_offs, (nv + 1 + pad) * d.off_bytes, s);
+    cudaError_t e = cudaSuccess;
+    if (hg::huge_allocation((nv + 1 + pad) * d.off_bytes + n * (d.key_bytes + d.val_bytes)))
+        e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&t->alloc_offs, (nv + 1 + pad) * d.off_bytes, s);
     if (e == cudaSuccess && n) e = cudaMallocAsync(&d.keys, n * d.key_bytes, s);
     if (e == cudaSuccess && n) e = cudaMallocAsync(&d.vals, n * d.val_bytes, s);
     if (e != cudaSuccess) {

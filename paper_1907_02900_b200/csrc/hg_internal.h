@@ -94,6 +94,7 @@ cudaError_t validate_table(const TableDesc& t, const void* input_keys, uint32_t*
 
 int num_sms();
 size_t smem_optin();  // opt-in shared memory per CTA (227 KB on B200)
+bool huge_allocation(uint64_t bytes);  // > 1/8 of device memory: drain the stream first
 
 // Vertex-space divisor of a table: global V (sharded) or V, with the shard base.
 inline uint64_t global_nv(const TableDesc& t) { return t.gnv ? t.gnv : t.nv; }

@@ -956,10 +956,11 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
 // Tables whose vertex range is too wide for the partitioned probe (its
 // offsets slice must fit shared memory within 2^16 partitions: V > 2^30 at
 // load 1, e.g. 2^31-key tables or C5's 2^32 vertices on one GPU): the probes
-// are routed into power-of-two vertex-range slices first (K11, hg_shard.cu;
-// keys only when counting, records {key, probe position} for per-probe
-// counts) and each slice is probed by the partitioned probe against its
-// view of the table (offsets of the slice's range, global entry positions).
+// are first split into power-of-two vertex-range slices (one pass of the
+// partition machinery; keys only when counting, records {key, probe
+// position} for per-probe counts) and each slice is probed by the
+// partitioned probe against its view of the table (offsets of the slice's
+// range, global entry positions).
 template <typename K, typename VT, typename OffT, typename IT, int POW2>
 static cudaError_t probe_sliced(const TableDesc& t, const ProbeArgs& a, uint32_t sshift,
                                 cudaStream_t s) {
@@ -968,20 +969,42 @@ static cudaError_t probe_sliced(const TableDesc& t, const ProbeArgs& a, uint32_t
     const uint64_t G = (t.nv + S - 1) / S;
     if (G > 256) return cudaErrorInvalidValue;
     const bool idx = a.counts != nullptr && a.counts_requested;
+    PartGeom sg;  // one split pass: "partition" = slice of 2^sshift vertices
+    sg.pshift = sshift;
+    sg.nparts = G;
+    sg.bits = sg.b1 = ceil_log2(G);
+    sg.b2 = 0;
     const size_t bytes = (a.m * (idx ? sizeof(E) : sizeof(K)) + 255) & ~size_t(255);
+    const size_t sbytes = ((G + 1) * 8 + 255) & ~size_t(255);
+    const size_t pbytes = idx ? PartitionScratch<K, IT, uint64_t>::bytes(sg, a.m)
+                              : PartitionScratch<K, void, uint64_t>::bytes(sg, a.m);
     char* scratch = nullptr;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes + 256 * 8, s);
+    cudaError_t e = cudaSuccess;
+    if (huge_allocation(bytes + sbytes + pbytes)) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes + sbytes + pbytes, s);
     if (e != cudaSuccess) return e;
-    uint64_t* dcnt = reinterpret_cast<uint64_t*>(scratch + bytes);
-    uint64_t cnt[256];
+    uint64_t* dstart = reinterpret_cast<uint64_t*>(scratch + bytes);
+    uint64_t cnt[257];
+    static const char* const kNames[3] = {"slice_hist", "slice_split", "slice_split2"};
     do {
-        e = route_keys(a.probes, sizeof(K), nullptr, sizeof(IT), a.m, 0, t.seed, t.hash_kind,
-                       global_nv(t), t.vbase, t.nv, S, uint32_t(G), idx ? nullptr : scratch,
-                       nullptr, dcnt, s, idx ? scratch : nullptr);
+        const Divisor nv = make_divisor(global_nv(t), t.vbase);
+        const K* probes = static_cast<const K*>(a.probes);
+        if (idx) {  // records {key, probe position}
+            e = partition<K, IT, uint64_t, POW2>(probes, static_cast<const IT*>(nullptr), a.m, t.seed,
+                                                 t.hash_kind, nv, sg, dstart,
+                                                 scratch + bytes + sbytes,
+                                                 reinterpret_cast<E*>(scratch), s, kNames);
+        } else {    // keys only
+            e = partition<K, void, uint64_t, POW2>(probes, static_cast<const void*>(nullptr), a.m,
+                                                   t.seed, t.hash_kind, nv, sg, dstart,
+                                                   scratch + bytes + sbytes,
+                                                   reinterpret_cast<K*>(scratch), s, kNames);
+        }
         if (e != cudaSuccess) break;
-        if ((e = cudaMemcpyAsync(cnt, dcnt, G * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        if ((e = cudaMemcpyAsync(cnt, dstart, (G + 1) * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
             (e = cudaStreamSynchronize(s)) != cudaSuccess)
             break;
+        for (uint64_t g = 0; g < G; ++g) cnt[g] = cnt[g + 1] - cnt[g];
         uint64_t start = 0;
         for (uint64_t g = 0; g < G && e == cudaSuccess; ++g) {
             TableDesc sub = t;

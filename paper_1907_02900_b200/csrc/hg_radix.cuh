@@ -200,8 +200,12 @@ k_part_hist(const In* __restrict__ keys, uint64_t n, uint64_t seed, int hk, Divi
 // ------------------------------------------------------------ multisplit
 
 constexpr int kSplitBlock = 512;
-constexpr int kSplitStages = 2;  // TMA input stages (one tile prefetched ahead)
+#ifndef HG_SPLIT_STAGES
+#define HG_SPLIT_STAGES 2
+#endif
+constexpr int kSplitStages = HG_SPLIT_STAGES;  // TMA input stages (one tile prefetched ahead)
 constexpr int kMaxDigits = 256;
+constexpr uint32_t kOwnerRun = 64;  // digit runs up to this long are filled by their owner
 // 4096-entry tiles for <= 8-byte entries, 2048 for 16-byte ones.
 template <typename E>
 __host__ __device__ constexpr int split_items() { return sizeof(E) >= 16 ? 4 : sizeof(E) <= 4 ? 16 : 8; }
@@ -256,6 +260,8 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
     __shared__ uint64_t s_t0[kSplitStages], s_t1[kSplitStages], s_cb[kSplitStages];
     __shared__ uint32_t s_ofs[kSplitStages], s_ok[kSplitStages];
     __shared__ uint32_t s_cnt[kMaxDigits];
+    __shared__ uint32_t s_long[kMaxDigits];  // digits whose run is filled cooperatively
+    __shared__ uint32_t s_nlong;
     __shared__ uint32_t s_off[kMaxDigits];
     // reserved global base - tile offset of each digit, in the offsets' width
     // (modular: base - off + j is the exact output index for j >= off)
@@ -326,6 +332,7 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
         const uint32_t cnt = uint32_t(s_t1[st] - t0);
         const uint64_t cbase = s_cb[st];
         for (uint32_t d = tid; d < ndig; d += kSplitBlock) s_cnt[d] = 0;
+        if (tid == 0) s_nlong = 0;
         mbar_wait(&s_bar[st], phase);
         const InT* src = reinterpret_cast<const InT*>(smem + st * L::kInBytes + s_ofs[st]);
         __syncthreads();
@@ -376,20 +383,37 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
             if (c) gb = atom_add(cursor + cbase + tid, OffT(c));
             // digit of every slot of this digit's run, written by the digit's
             // owner as a byte run (word stores in the middle) instead of one
-            // random byte store per entry in the scatter
-            uint32_t o = off;
-            const uint32_t e = off + c;
-            const uint8_t dd = uint8_t(tid);
-            while (o < e && (o & 3)) s_dig[o++] = dd;
-            const uint32_t w4 = uint32_t(dd) * 0x01010101u;
-            for (; o + 4 <= e; o += 4) *reinterpret_cast<uint32_t*>(s_dig + o) = w4;
-            while (o < e) s_dig[o++] = dd;
+            // random byte store per entry in the scatter; runs longer than
+            // kOwnerRun (skewed keys) are filled by the whole CTA below
+            if (c <= kOwnerRun) {
+                uint32_t o = off;
+                const uint32_t e = off + c;
+                const uint8_t dd = uint8_t(tid);
+                while (o < e && (o & 3)) s_dig[o++] = dd;
+                const uint32_t w4 = uint32_t(dd) * 0x01010101u;
+                for (; o + 4 <= e; o += 4) *reinterpret_cast<uint32_t*>(s_dig + o) = w4;
+                while (o < e) s_dig[o++] = dd;
+            } else {
+                s_long[atomicAdd(&s_nlong, 1u)] = tid;
+            }
         }
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
             const uint32_t j = tid + k * kSplitBlock;
             if (j < cnt) s_ent[s_off[dr[k] >> 16] + (dr[k] & 0xFFFFu)] = ent[k];
+        }
+        for (uint32_t li = 0; li < s_nlong; ++li) {
+            const uint32_t d = s_long[li];
+            const uint32_t o = s_off[d], e = o + s_cnt[d];
+            const uint32_t w0 = (o + 3) >> 2, w1 = e >> 2;  // whole words inside the run
+            const uint32_t w4 = d * 0x01010101u;
+            for (uint32_t w = w0 + tid; w < w1; w += kSplitBlock)
+                reinterpret_cast<uint32_t*>(s_dig)[w] = w4;
+            if (tid < 4) {
+                if (o + tid < 4 * w0) s_dig[o + tid] = uint8_t(d);
+                if (4 * w1 + tid < e) s_dig[4 * w1 + tid] = uint8_t(d);
+            }
         }
         if (c) s_gbo[tid] = gb - OffT(off);
         __syncthreads();
