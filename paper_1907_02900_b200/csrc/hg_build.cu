@@ -337,7 +337,15 @@ static uint32_t v2_slice_shift(const TableDesc& t, const BuildArgs& a, size_t en
         const double per_vertex = double(t.n) / double(t.nv);
         while (ps < kMaxPartShift && per_vertex * double(uint64_t(2) << ps) <= target) ++ps;
     }
-    return ceil_log2(t.nv) > 16 + ps ? 16 + ps : 0;
+    // Slice when 2^16 partitions would be wider than kMaxPartShift, or hold
+    // more than 4x the tuned entry count (oversized partitions go through
+    // the grid-wide K7b path, which beats an extra split pass up to ~4x:
+    // C3 u64 at load 1 runs 2x-oversized partitions).
+    // A requested partition width (partition_vertices) is kept exactly.
+    const uint32_t vbits = ceil_log2(t.nv);
+    const uint32_t slack = a.partition_vertices ? 0 : 2;
+    if (vbits > 16 + kMaxPartShift || vbits > 16 + ps + slack) return 16 + ps;
+    return 0;
 }
 
 // Binned build over a vertex range wider than 2^16 partitions of the tuned

@@ -235,6 +235,92 @@ struct ProbeLayout {
     }
 };
 
+// ------------------------------------------------ heavy segments (skew)
+// A probe whose segment is longer than kHeavySeg (a heavy key of a skewed
+// table, e.g. C3's Zipf ranks: millions of entries under one vertex) would
+// keep one warp of one CTA busy for the whole walk while the rest of the GPU
+// idles. k_probe_part queues such walks instead as work items of at most
+// kHeavyChunk comparisons, and k_heavy_walk runs them on the whole grid:
+// one CTA per item, coalesced key loads, one atomic per item.
+constexpr uint64_t kHeavySeg = uint64_t(1) << 13;
+constexpr uint32_t kHeavyChunk = 1u << 15;
+
+struct HeavyItem {
+    uint64_t key;
+    uint64_t begin;  // first table entry (global index) of the chunk
+    uint64_t pidx;   // probe position (per-probe counts)
+    uint32_t len;    // comparisons in the chunk (0: unused slot)
+    uint32_t pad;
+};
+
+struct HeavyQueue {
+    HeavyItem* items = nullptr;  // nullptr: walk every segment in place
+    uint32_t* n = nullptr;
+    uint32_t cap = 0;
+};
+
+// Warp-collective: queues the segment [gb, gb + len) of probe (key, pidx) as
+// chunks and returns true, or returns false (the warp walks it itself) when
+// it is short or the queue is full. Slots reserved past a full queue's end
+// are never read (k_heavy_walk stops at cap); reserved slots below it are
+// always written.
+template <typename K>
+__device__ __forceinline__ bool defer_heavy(const HeavyQueue& q, K key, uint64_t gb, uint64_t len,
+                                            uint64_t pidx) {
+    if (q.items == nullptr || len <= kHeavySeg) return false;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nch = uint32_t((len + kHeavyChunk - 1) / kHeavyChunk);
+    uint32_t slot = 0;
+    if (lane == 0) slot = atomicAdd(q.n, nch);
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    const bool ok = uint64_t(slot) + nch <= q.cap;
+    for (uint32_t c = lane; c < nch && slot + c < q.cap; c += 32) {
+        HeavyItem it;
+        it.key = uint64_t(key);
+        it.begin = gb + uint64_t(c) * kHeavyChunk;
+        it.pidx = pidx;
+        it.len = ok ? uint32_t(len - uint64_t(c) * kHeavyChunk < kHeavyChunk
+                                   ? len - uint64_t(c) * kHeavyChunk : kHeavyChunk)
+                    : 0u;
+        it.pad = 0;
+        q.items[slot + c] = it;
+    }
+    return ok;
+}
+
+constexpr int kHeavyBlock = 512;
+
+// Matches go to totals[0] and, with COUNTS, to counts[pidx] (per-probe
+// counts in probe order).
+template <typename K, bool COUNTS>
+__global__ void __launch_bounds__(kHeavyBlock)
+k_heavy_walk(const HeavyItem* __restrict__ items, const uint32_t* __restrict__ n_items, uint32_t cap,
+             const K* __restrict__ tkeys, uint64_t* __restrict__ totals,
+             uint32_t* __restrict__ counts) {
+    __shared__ uint32_t s_w[kHeavyBlock / 32];
+    const uint32_t n = *n_items < cap ? *n_items : cap;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const HeavyItem it = items[i];
+        const K key = K(it.key);
+        const K* kp = tkeys + it.begin;
+        uint32_t c = 0;
+        for (uint32_t t = threadIdx.x; t < it.len; t += kHeavyBlock) c += kp[t] == key;
+        c = warp_sum(c);
+        if (lane == 0) s_w[warp] = c;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t x = lane < kHeavyBlock / 32 ? s_w[lane] : 0;
+            x = warp_sum(x);
+            if (lane == 0 && x) {
+                if constexpr (COUNTS) atomicAdd(counts + it.pidx, x);
+                atomicAdd(reinterpret_cast<unsigned long long*>(totals), (unsigned long long)x);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // MODE 0: totals only; 1: totals + per-probe count at the probe's partitioned
 // position (pcount[pos]) or, with ORIG, at its original index; 2: pairs.
 // One partition per CTA iteration: thread 0 issues TMA bulk loads of the
@@ -243,14 +329,14 @@ struct ProbeLayout {
 // memory. Slices larger than the caps are read from global memory instead.
 template <typename K, typename VT, typename OffT, typename IT, int POW2, int MODE, bool ORIG,
           typename PT>
-__global__ void __launch_bounds__(kPartProbeBlock)
+__global__ void __launch_bounds__(kPartProbeBlock, (MODE == 2 ? 2 : 3))
 k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __restrict__ ppart,
              uint64_t nparts, uint64_t nv_total, uint64_t seed, int hk, Divisor nv,
              uint32_t pshift, const OffT* __restrict__ offs, const K* __restrict__ tkeys,
              const VT* __restrict__ tvals, uint32_t kcap, uint32_t pcap,
              uint32_t* __restrict__ pcount, const uint64_t* __restrict__ pair_off,
              void* __restrict__ pairs, uint64_t cap, uint64_t* __restrict__ totals,
-             uint32_t* ticket) {
+             uint32_t* ticket, HeavyQueue heavy) {
     using PE = EntryT<K, IT>;
     using PEnt = typename PE::T;
     using L = ProbeLayout<K, OffT, PEnt>;
@@ -342,6 +428,7 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
                         const I kb = __shfl_sync(0xffffffffu, b, src);
                         const I ke = __shfl_sync(0xffffffffu, e, src);
                         const K kk = __shfl_sync(0xffffffffu, key, src);
+                        if (defer_heavy(heavy, kk, tb + uint64_t(kb), uint64_t(ke - kb), 0)) continue;
                         uint32_t cc = 0;
                         for (I t = kb + I(lane); t < ke; t += 32) cc += kp[t] == kk;
                         cc = warp_sum(cc);
@@ -375,6 +462,12 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
                         const uint64_t kb = __shfl_sync(0xffffffffu, b, src);
                         const uint64_t ke = __shfl_sync(0xffffffffu, e, src);
                         const K kk = __shfl_sync(0xffffffffu, key, src);
+                        if constexpr (MODE == 1 && ORIG) {
+                            // the deferred walk adds to counts[pidx] (and the totals below)
+                            if (defer_heavy(heavy, kk, tb + kb, ke - kb,
+                                            uint64_t(__shfl_sync(0xffffffffu, pidx, src))))
+                                continue;
+                        }
                         uint32_t cc = 0;
                         for (uint64_t t = kb + lane; t < ke; t += 32) cc += kp[t] == kk;
                         cc = warp_sum(cc);
@@ -816,8 +909,13 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
     const size_t po_bytes = single ? ((g.nparts * 8 + 255) & ~size_t(255))
                                    : a.pairs ? (((a.m + 1) * 8 + 255) & ~size_t(255)) : 0;
     const size_t scan_bytes = (a.pairs && !single) ? ((scan_scratch_bytes(a.m) + 255) & ~size_t(255)) : 0;
+    // heavy-segment queue (count-only and per-probe counts): 2^20 items, 32 MB
+    const bool use_heavy = !a.pairs;
+    const uint32_t hcap = use_heavy ? (1u << 20) : 0;
+    const size_t heavy_bytes = size_t(hcap) * sizeof(HeavyItem);
     if ((e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
-                             ps_bytes + pscr + reorg_bytes + cnt_bytes + po_bytes + scan_bytes + 256,
+                             ps_bytes + pscr + reorg_bytes + cnt_bytes + po_bytes + scan_bytes +
+                                 heavy_bytes + 256,
                              s)) != cudaSuccess)
         return e;
     char* cur = scratch;
@@ -833,7 +931,28 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
     cur += po_bytes;
     void* scan_scr = cur;
     cur += scan_bytes;
-    uint32_t* ticket = reinterpret_cast<uint32_t*>(cur);
+    HeavyQueue hq;
+    if (use_heavy) {
+        hq.items = reinterpret_cast<HeavyItem*>(cur);
+        cur += heavy_bytes;
+        hq.cap = hcap;
+    }
+    uint32_t* ticket = reinterpret_cast<uint32_t*>(cur);  // ticket, heavy count
+    if (use_heavy) hq.n = ticket + 1;
+    // deferred heavy walks, after the partitioned kernel (per-probe counts: COUNTS)
+    auto run_heavy = [&](bool counts) -> cudaError_t {
+        const unsigned gh = unsigned(num_sms() * 2);
+        if (counts) {
+            HG_LAUNCH("k8h_heavy_walk", s,
+                      (k_heavy_walk<K, true><<<gh, kHeavyBlock, 0, s>>>(hq.items, hq.n, hq.cap, tkeys,
+                                                                        a.totals, a.counts)));
+        } else {
+            HG_LAUNCH("k8h_heavy_walk", s,
+                      (k_heavy_walk<K, false><<<gh, kHeavyBlock, 0, s>>>(hq.items, hq.n, hq.cap,
+                                                                         tkeys, a.totals, nullptr)));
+        }
+        return cudaGetLastError();
+    };
     do {
         if (need_idx) {
             e = partition<K, IT, OffT, POW2>(probes, static_cast<const IT*>(nullptr), a.m, t.seed,
@@ -856,12 +975,12 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPartProbeBlock, smem);
             const unsigned gk = unsigned(
                 std::min<uint64_t>(uint64_t(std::max(1, per_sm)) * sms, g.nparts));
-            if ((r = cudaMemsetAsync(ticket, 0, 4, s)) != cudaSuccess) return r;
+            if ((r = cudaMemsetAsync(ticket, 0, 8, s)) != cudaSuccess) return r;
             HG_LAUNCH(name, s,
                       kern<<<gk, kPartProbeBlock, smem, s>>>(
                           static_cast<const E1*>(reorg), ppart, g.nparts, t.nv, t.seed,
                           t.hash_kind, nv, g.pshift, offs, tkeys, tvals, kcap, pcap, pc, po, pr,
-                          cap, a.totals, ticket));
+                          cap, a.totals, ticket, (pc == a.counts && pc) ? hq : HeavyQueue{}));
             return cudaGetLastError();
         };
         // the pairs kernel reads its probe entries straight from global memory
@@ -897,19 +1016,21 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPartProbeBlock, smem0);
             const unsigned gk = unsigned(
                 std::min<uint64_t>(uint64_t(std::max(1, per_sm)) * sms, g.nparts));
-            if ((e = cudaMemsetAsync(ticket, 0, 4, s)) != cudaSuccess) break;
+            if ((e = cudaMemsetAsync(ticket, 0, 8, s)) != cudaSuccess) break;
             HG_LAUNCH("k8p_probe_part", s,
                       kern<<<gk, kPartProbeBlock, smem0, s>>>(
                           static_cast<const E0*>(reorg), ppart, g.nparts, t.nv, t.seed,
                           t.hash_kind, nv, g.pshift, offs, tkeys, tvals, kcap, pcap, nullptr,
-                          nullptr, nullptr, 0, a.totals, ticket));
-            e = cudaGetLastError();
+                          nullptr, nullptr, 0, a.totals, ticket, hq));
+            if ((e = cudaGetLastError()) != cudaSuccess) break;
+            e = run_heavy(false);
             break;
         }
         if (!a.pairs) {
             // per-probe counts in the caller's (original) order
             e = launch(k_probe_part<K, VT, OffT, IT, POW2, 1, true, uint32_t>, "k8p_probe_part",
                        a.counts, nullptr, nullptr, 0);
+            if (e == cudaSuccess) e = run_heavy(true);
             break;
         }
         if (single) {

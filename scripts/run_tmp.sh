@@ -1,4 +1,3 @@
-BENCH_DEBUG=x timeout 900 python bench.py --config c5 --steps 4 --warmup 3 > gpurun_out/bench_c5_x.json 2> gpurun_out/bench_c5_x.err
-grep "step host" gpurun_out/bench_c5_x.err
-timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-extras --no-e2e --csv= > gpurun_out/b.json 2>/dev/null
-python -c "import json;d=json.load(open('gpurun_out/b.json'));print(d['value'],d['ms_per_step'])"
+timeout 600 python scripts/prof_c3.py 28 > gpurun_out/c3prof.log 2>&1
+head -2 gpurun_out/c3prof.log
+timeout 900 python -m pytest tests/test_gpu_sliced.py tests/test_gpu_configs.py -q -x 2>&1 | tail -3

@@ -183,3 +183,37 @@ def test_u64_probe_counts_many_probes(oracle, cuda):
     hg.probe_device(t, probes[:sub], r2, counts=c2)
     ro = oracle.probe_standard(o, hp)
     assert [int(x) for x in r2.tolist()] == [ro["match_count"], ro["key_comparisons"]]
+
+
+@pytest.mark.parametrize("width", [4, 8])
+def test_heavy_segments_deferred(oracle, cuda, width):
+    """Segments longer than kHeavySeg (8192 entries: heavy keys of a skewed
+    table) are queued by the partitioned probe and walked by the whole grid
+    (k_heavy_walk): totals and per-probe counts equal the oracle's, including
+    a queue item per 2^15 comparisons of a 300000-entry segment."""
+    rng = np.random.default_rng(width)
+    n = 1 << 22
+    keys = rng.integers(0, 1 << 31, size=n, dtype=np.uint64)
+    keys[:300000] = 777                      # one very heavy key
+    keys[300000:340000] = rng.integers(1000, 1004, size=40000, dtype=np.uint64)  # 4 x ~10000
+    dt = np.uint32 if width == 4 else np.uint64
+    t = hg.build_v2(keys.astype(dt))
+    m = 1 << 21
+    probes = rng.integers(0, 1 << 31, size=m, dtype=np.uint64)
+    probes[2::7] = keys[2::7][: len(probes[2::7])]
+    probes[1::101] = 1001
+    probes[::97] = 777
+    dp = cuda.from_numpy(probes.astype(dt).view(np.int32 if width == 4 else np.int64)).cuda()
+    o = oracle.build(keys, variant=2)
+    ro = oracle.probe_standard(o, probes)
+    res = cuda.zeros(2, dtype=cuda.int64, device="cuda")
+    hg.probe_device(t, dp, res, method=2)
+    assert [int(x) for x in res.tolist()] == [ro["match_count"], ro["key_comparisons"]]
+    counts = cuda.zeros(m, dtype=cuda.int32, device="cuda")
+    res.zero_()
+    hg.probe_device(t, dp, res, counts=counts, method=2)
+    assert [int(x) for x in res.tolist()] == [ro["match_count"], ro["key_comparisons"]]
+    hc = counts.cpu().numpy()
+    assert hc[::97].tolist() == [300000] * len(hc[::97])
+    for j in (1, 102, 2, 9, 5):
+        assert int(hc[j]) == oracle.count_instances(o, int(probes[j]))
