@@ -232,7 +232,8 @@ hg_status hg_shard_range(uint64_t global_vertices, uint32_t shards, uint32_t sha
  * out_keys/out_vals (n entries each, keys of shard 0 first) and writes the
  * per-shard counts to shard_counts (G entries; host or device). Values are
  * vals[i] or, when vals is NULL, val_base + i (global input positions) of
- * width val_width. G <= 256. */
+ * width val_width; out_vals may be NULL (keys only, e.g. count-only probes).
+ * G <= 256. */
 hg_status hg_route(const void* keys, int32_t key_width, const void* vals, int32_t val_width,
                    uint64_t n, uint64_t val_base, uint64_t hash_seed, int32_t hash_kind,
                    uint64_t global_vertices, uint32_t shards, void* out_keys, void* out_vals,

@@ -812,8 +812,8 @@ hg_status hg_route(const void* keys, int32_t key_width, const void* vals, int32_
     if (hash_kind != HG_HASH_MIX64 && hash_kind != HG_HASH_IDENTITY)
         return fail(HG_EINVAL, "unknown hash_kind");
     if (!shard_counts) return fail(HG_EINVAL, "shard_counts is NULL");
-    if (n && (!is_device_ptr(keys) || !is_device_ptr(out_keys) || !is_device_ptr(out_vals) ||
-              (vals && !is_device_ptr(vals))))
+    if (n && (!is_device_ptr(keys) || !is_device_ptr(out_keys) ||
+              (out_vals && !is_device_ptr(out_vals)) || (vals && !is_device_ptr(vals))))
         return fail(HG_EINVAL, "hg_route takes device buffers");
     int dev = 0;
     if (hg_status st = need_device(&dev); st != HG_OK) return st;

@@ -242,7 +242,8 @@ constexpr int split_min_blocks() {
 
 template <typename K, typename VT, typename OffT, bool RAW, bool PASS2, int POW2>
 __global__ void __launch_bounds__(kSplitBlock, (split_min_blocks<K, VT, RAW>()))
-k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t n, uint64_t seed,
+k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t val_base,
+             uint64_t n, uint64_t seed,
              int hk, Divisor nv, uint32_t pshift, uint32_t dshift, uint32_t dmask, uint32_t b2,
              OffT* __restrict__ cursor, const OffT* __restrict__ part_start, uint32_t nb1,
              const uint64_t* __restrict__ tile_prefix, uint64_t ntiles, uint64_t nparts,
@@ -347,7 +348,7 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
                 if constexpr (RAW) {
                     key = src[j];
                     if constexpr (ET::kHasVal) {
-                        ent[k] = ET::make(key, vals ? VT(vals[t0 + j]) : VT(t0 + j));
+                        ent[k] = ET::make(key, vals ? VT(vals[t0 + j]) : VT(val_base + t0 + j));
                     } else {
                         ent[k] = ET::make(key, 0);
                     }
@@ -476,7 +477,7 @@ template <typename K, typename VT, typename OffT, int POW2>
 cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, int hk,
                       const Divisor& nv, const PartGeom& g, OffT* part_start, void* scratch,
                       typename EntryT<K, VT>::T* out, cudaStream_t s, const char* const names[3],
-                      const typename EntryT<K, VT>::T* rec = nullptr) {
+                      const typename EntryT<K, VT>::T* rec = nullptr, uint64_t val_base = 0) {
     using PS = PartitionScratch<K, VT, OffT>;
     using E = typename EntryT<K, VT>::T;
     char* p = static_cast<char*>(scratch);
@@ -550,20 +551,20 @@ cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, 
         // single pass straight into partition order
         HG_LAUNCH(names[1], s,
                   (ks1<<<g1, kSplitBlock, sm1, s>>>(
-                      in1, vals, n, seed, hk, nv, g.pshift, 0, uint32_t((1u << g.b1) - 1), 0,
-                      cur2, part_start, 0, nullptr, tiles1, g.nparts, out)));
+                      in1, vals, val_base, n, seed, hk, nv, g.pshift, 0, uint32_t((1u << g.b1) - 1),
+                      0, cur2, part_start, 0, nullptr, tiles1, g.nparts, out)));
         return cudaGetLastError();
     }
     HG_LAUNCH(names[1], s,
               (ks1<<<g1, kSplitBlock, sm1, s>>>(
-                  in1, vals, n, seed, hk, nv, g.pshift, g.b2, uint32_t((1u << g.b1) - 1), 0, cur1,
-                  part_start, 0, nullptr, tiles1, g.nparts, mid)));
+                  in1, vals, val_base, n, seed, hk, nv, g.pshift, g.b2, uint32_t((1u << g.b1) - 1), 0,
+                  cur1, part_start, 0, nullptr, tiles1, g.nparts, mid)));
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     k_tile_prefix<OffT><<<1, 32, 0, s>>>(part_start, g.nparts, nb1, g.b2, kSplitTile, tile_prefix);
     const uint64_t tiles2 = tiles1 + nb1;  // upper bound; exact count = tile_prefix[nb1]
     HG_LAUNCH(names[2], s,
               (ks2<<<g2, kSplitBlock, sm2, s>>>(
-                  mid, nullptr, n, seed, hk, nv, g.pshift, 0, uint32_t((1u << g.b2) - 1), g.b2,
+                  mid, nullptr, 0, n, seed, hk, nv, g.pshift, 0, uint32_t((1u << g.b2) - 1), g.b2,
                   cur2, part_start, nb1, tile_prefix, tiles2, g.nparts, out)));
     return cudaGetLastError();
 }

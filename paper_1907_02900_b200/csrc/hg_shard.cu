@@ -180,6 +180,46 @@ static cudaError_t route_impl(const void* keys, const void* vals, uint64_t n, ui
     return e;
 }
 
+template <typename OffT>
+__global__ void k_split_counts(const OffT* __restrict__ start, uint32_t G,
+                               unsigned long long* __restrict__ counts) {
+    for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) counts[g] = start[g + 1] - start[g];
+}
+
+// Power-of-two spans (owner = local vertex >> log2(span): V and G powers of
+// two, e.g. the weak-scaling C2 and strong-scaling C5 configs) route with one
+// pass of the partition machinery (hg_radix.cuh: TMA-staged tiles, shared-
+// memory ranking, coalesced runs) instead of K11: records {key, val_base + i}
+// or bare keys grouped by owner, counts from the owner starts.
+template <typename K, typename VT, int HM>
+static cudaError_t route_split(const void* keys, uint64_t n, uint64_t val_base, uint64_t seed,
+                               int hash_kind, const Divisor& gv, uint32_t sshift, uint32_t G,
+                               void* out, uint64_t* shard_counts, cudaStream_t s) {
+    PartGeom g;
+    g.pshift = sshift;
+    g.nparts = G;
+    g.bits = g.b1 = ceil_log2(G);
+    g.b2 = 0;
+    const size_t sbytes = ((G + 1) * 8 + 255) & ~size_t(255);
+    const size_t pbytes = PartitionScratch<K, VT, uint64_t>::bytes(g, n);
+    char* scr = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scr), sbytes + pbytes, s);
+    if (e != cudaSuccess) return e;
+    static const char* const kNames[3] = {"k11_route_hist", "k11_route_split", "-"};
+    uint64_t* start = reinterpret_cast<uint64_t*>(scr);
+    e = partition<K, VT, uint64_t, HM>(static_cast<const K*>(keys), static_cast<const VT*>(nullptr),
+                                       n, seed, hash_kind, gv, g, start, scr + sbytes,
+                                       static_cast<typename EntryT<K, VT>::T*>(out), s, kNames,
+                                       nullptr, val_base);
+    if (e == cudaSuccess) {
+        k_split_counts<uint64_t><<<1, 256, 0, s>>>(start, G,
+                                                   reinterpret_cast<unsigned long long*>(shard_counts));
+        e = cudaGetLastError();
+    }
+    cudaFreeAsync(scr, s);
+    return e;
+}
+
 template <typename K, typename VT>
 static cudaError_t route_hash_typed(const void* keys, const void* vals, uint64_t n, uint64_t val_base,
                                     uint64_t seed, int hash_kind, uint64_t V, uint64_t vbase,
@@ -187,9 +227,19 @@ static cudaError_t route_hash_typed(const void* keys, const void* vals, uint64_t
                                     void* out_vals, void* out_rec, uint64_t* shard_counts,
                                     cudaStream_t s) {
     const Divisor gv = make_divisor(V, vbase);  // (h mod V) - vbase
-    const Divisor sp = make_divisor(span ? span : (nloc + G - 1) / G);
+    const uint64_t spv = span ? span : (nloc + G - 1) / G;
+    const Divisor sp = make_divisor(spv);
+    const bool split = sp.pow2 && vals == nullptr && (out_rec || out_vals == nullptr) && n &&
+                       G <= 256 && (uint64_t(G) << sp.shift) >= nloc;
     return dispatch_hash_mode(hash_mode(V, hash_kind), [&](auto m) {
         constexpr int HM = decltype(m)::value;
+        if (split) {
+            if (out_rec)
+                return route_split<K, VT, HM>(keys, n, val_base, seed, hash_kind, gv, sp.shift, G,
+                                              out_rec, shard_counts, s);
+            return route_split<K, void, HM>(keys, n, 0, seed, hash_kind, gv, sp.shift, G, out_keys,
+                                            shard_counts, s);
+        }
         const OwnHash<HM> own{seed, gv, sp};
         return out_rec ? route_impl<K, VT, OwnHash<HM>, true>(keys, vals, n, val_base, own, G, nullptr,
                                                              nullptr, out_rec, shard_counts, s)

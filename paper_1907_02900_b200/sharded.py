@@ -61,18 +61,19 @@ class CudaEngine:
         return t.empty(n, dtype=t.int32 if width == 4 else t.int64, device="cuda")
 
     def route(self, keys, vals, val_width: int, val_base: int, seed: int, hash_kind: int,
-              global_vertices: int, shards: int):
+              global_vertices: int, shards: int, keys_only: bool = False):
         t = self.torch
         ka = _Arr(keys)
         n = ka.n
         out_k = self.empty(n, ka.width)
-        out_v = self.empty(n, val_width)
+        out_v = None if keys_only else self.empty(n, val_width)
         counts = t.zeros(shards, dtype=t.int64, device="cuda")
         va = _Arr(vals) if vals is not None else None
         s = t.cuda.current_stream().cuda_stream
         _check(_lib.lib().hg_route(ka.ptr, ka.width, va.ptr if va else None, val_width, n,
                                    val_base, seed, hash_kind, global_vertices, shards,
-                                   out_k.data_ptr(), out_v.data_ptr(), counts.data_ptr(), s))
+                                   out_k.data_ptr(), out_v.data_ptr() if out_v is not None else None,
+                                   counts.data_ptr(), s))
         return out_k, out_v, counts
 
     def build(self, keys, vals, global_vertices: int, base: int, count: int, cfg: BuildConfig,
@@ -289,7 +290,8 @@ class ShardedHashGraph:
         travel (count-only needs no positions)."""
         st = self.table
         send_k, _, counts = self.engine.route(probes, None, 4, global_offset, self.hash_seed,
-                                              self.hash_kind, st.global_vertices, self.world)
+                                              self.hash_kind, st.global_vertices, self.world,
+                                              keys_only=True)
         M = self._count_matrix(counts)
         recv_k = self._alltoall(send_k, M)
         self.last_local_m = int(recv_k.numel())

@@ -217,3 +217,27 @@ def test_heavy_segments_deferred(oracle, cuda, width):
     assert hc[::97].tolist() == [300000] * len(hc[::97])
     for j in (1, 102, 2, 9, 5):
         assert int(hc[j]) == oracle.count_instances(o, int(probes[j]))
+
+
+@pytest.mark.parametrize("G,V", [(4, 1 << 20), (8, 1 << 21), (2, 1 << 20), (1, 1 << 20)])
+def test_route_records_split_path(cuda, G, V):
+    """Power-of-two spans route with the partition machinery (one TMA-staged
+    split pass); the groups equal K11's (the SoA route) as (key, position)
+    multisets, counts included, and keys-only routing returns the same keys."""
+    from paper_1907_02900_b200.sharded import CudaEngine
+    n = (1 << 20) + 77
+    keys = cuda.empty(n, dtype=cuda.int32, device="cuda")
+    hg.generate(keys, kind=0, seed=17)
+    eng = CudaEngine(2)
+    sk, sv, c1 = eng.route(keys, None, 4, 5000, 0, 0, V, G)           # K11 (SoA with values)
+    rec, c2 = eng.route_records(keys, 4, 5000, 0, 0, V, G)            # split path
+    ko, _, c3 = eng.route(keys, None, 4, 0, 0, 0, V, G, keys_only=True)  # split path, keys only
+    assert c1.tolist() == c2.tolist() == c3.tolist()
+    rk, rv = eng.unpack_records(rec, 4, 4)
+    start = 0
+    for g, c in enumerate(c1.tolist()):
+        a = np.stack([sk[start:start + c].cpu().numpy(), sv[start:start + c].cpu().numpy()], 1)
+        b = np.stack([rk[start:start + c].cpu().numpy(), rv[start:start + c].cpu().numpy()], 1)
+        assert (a[np.lexsort(a.T[::-1])] == b[np.lexsort(b.T[::-1])]).all(), f"group {g}"
+        assert (np.sort(ko[start:start + c].cpu().numpy()) == np.sort(a[:, 0])).all()
+        start += c

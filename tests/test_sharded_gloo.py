@@ -20,7 +20,7 @@ class NumpyEngine:
         from oracle.oracle import Oracle
         self.o = Oracle()
 
-    def route(self, keys, vals, val_width, val_base, seed, hash_kind, V, G):
+    def route(self, keys, vals, val_width, val_base, seed, hash_kind, V, G, keys_only=False):
         k = keys.numpy().astype(np.uint64) if keys.dtype == torch.int64 else \
             keys.numpy().view(np.uint32).astype(np.uint64)
         v = self.o.vertices(k, seed, V, hash_kind)
