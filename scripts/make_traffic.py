@@ -1,8 +1,9 @@
-"""Writes profiles/traffic.json (DRAM bytes per launch from one ncu --set full
-capture per kernel, as bench.py's roofline.traffic) and the round's ncu
-summary from gpurun_out/full_*_raw.csv (scripts/gpu_prof.sh).
+"""Writes profiles/traffic.json (DRAM bytes per launch from an ncu --set full
+capture, as bench.py's roofline.traffic) and the round's ncu summary.
 
-    python scripts/make_traffic.py r01
+    python scripts/make_traffic.py r02    # gpurun_out/r02_full_raw.csv (gpu_prof.sh):
+                                          # the 8 kernels of one C2 step, launch order
+    python scripts/make_traffic.py r01    # round-1 layout: gpurun_out/full_*_raw.csv
 """
 import csv
 import json
@@ -25,9 +26,13 @@ KEEP = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
         "sm__warps_active.avg.pct_of_peak_sustained_active"]
+if os.path.exists(os.path.join(OUT, f"{tag}_full_raw.csv")):
+    # one capture of a whole C2 step: build (K4, K6a, K6b, K7), probe (P4, P6a, P6b, K8p)
+    ROWS = {f"{tag}_full": ["k4_part_hist", "k6a_multisplit", "k6b_multisplit", "k7_part_build",
+                            "p4_part_hist", "p6a_multisplit", "p6b_multisplit", "k8p_probe_part"]}
 traffic, summary = {}, []
 for cap, names in ROWS.items():
-    path = os.path.join(OUT, f"full_{cap}_raw.csv")
+    path = os.path.join(OUT, f"{cap}_raw.csv" if cap.endswith("_full") else f"full_{cap}_raw.csv")
     if not os.path.exists(path):
         continue
     rows = list(csv.reader(open(path)))
