@@ -319,6 +319,35 @@ __device__ __forceinline__ uint32_t eq_and(K x, K y, bool in) {
     return d;
 }
 
+// seg_count that also reports, in `pos`, the index of a match inside the
+// segment (the only one when the count is 1): the single-pass pairs kernel
+// needs it for its one-match fast path and no longer walks the segment again.
+template <typename K>
+__device__ __forceinline__ uint32_t seg_count_pos(const K* __restrict__ sp, uint64_t len, K key,
+                                                  uint32_t& pos) {
+    if (len <= 4) {
+        uint32_t neg = 0, at = 0;
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) {
+            const bool in = q < len;
+            const K x = in ? sp[q] : K(0);
+            const uint32_t eq = eq_and(x, key, in);
+            neg += eq;
+            at |= eq & q;
+        }
+        pos = at;
+        return 0u - neg;
+    }
+    uint32_t c = 0, at = 0;
+    for (uint32_t t = 0; t < uint32_t(len); ++t) {
+        const bool eq = sp[t] == key;
+        c += eq;
+        at = eq ? t : at;
+    }
+    pos = at;
+    return c;
+}
+
 // Matches of `key` in the segment sp[0, len) for a short segment (the caller
 // walks long ones warp-cooperatively). Segments of <= 4 entries (~99% at load
 // 1) use a fixed, predicated 4-wide compare: no loop, no divergence.

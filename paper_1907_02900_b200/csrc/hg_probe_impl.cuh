@@ -560,7 +560,8 @@ template <typename K, typename OffT, typename PEnt, typename PE, int POW2>
 __device__ __forceinline__ uint32_t pair_count(const K* __restrict__ kp, const PEnt& ent,
                                                const OffT* soff, uint64_t i, uint64_t qn, uint64_t tb,
                                                uint64_t vb, uint64_t seed, int hk, const Divisor& nv,
-                                               uint64_t& compared, K& key, uint64_t& b, uint64_t& e) {
+                                               uint64_t& compared, K& key, uint64_t& b, uint64_t& e,
+                                               uint32_t& pos) {
     // partition-relative positions in the offsets' width (u32 at C2)
     using I = OffT;
     const uint32_t lane = threadIdx.x & 31;
@@ -575,7 +576,8 @@ __device__ __forceinline__ uint32_t pair_count(const K* __restrict__ kp, const P
     const I len = ei - bi;
     compared += len;
     uint32_t c = 0;
-    if (len <= I(kLongSeg)) c = seg_count(kp + bi, uint64_t(len), key);
+    pos = 0;
+    if (len <= I(kLongSeg)) c = seg_count_pos(kp + bi, uint64_t(len), key, pos);
     uint32_t longm = __ballot_sync(0xffffffffu, len > I(kLongSeg));
     while (longm) {
         const int src = __ffs(longm) - 1;
@@ -596,16 +598,11 @@ __device__ __forceinline__ uint32_t pair_count(const K* __restrict__ kp, const P
 constexpr uint32_t kNeedWalk = 0xFFFFFFFFu;
 
 // Pass-A summary of one probe for pass B: 0 (no match), (t << 16) | 1 (one
-// match at tile key t, short segment, t < 2^16) or kNeedWalk.
-template <typename K>
-__device__ __forceinline__ uint32_t pair_info(const K* __restrict__ kp, K key, uint64_t b, uint64_t e,
-                                              uint32_t c) {
+// match at tile key t = b + pos, short segment, t < 2^16) or kNeedWalk.
+__device__ __forceinline__ uint32_t pair_info(uint64_t b, uint64_t e, uint32_t c, uint32_t pos) {
     if (c == 0) return 0u;
     if (c != 1 || e - b > kLongSeg || e > 0xFFFFu) return kNeedWalk;
-    uint32_t th = uint32_t(b);
-    for (uint64_t t = b; t < e; ++t)
-        if (kp[t] == key) th = uint32_t(t);
-    return (th << 16) | 1u;
+    return (uint32_t(b + pos) << 16) | 1u;
 }
 
 template <typename K, typename VT, typename OffT, typename IT, int POW2, typename PT>
@@ -697,12 +694,13 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
                 const uint64_t i = ch * kPartProbeBlock + i0;
                 const PEnt cur = nxt;  // entries are prefetched one chunk ahead
                 if (i + kPartProbeBlock < qn) nxt = ep[i + kPartProbeBlock];
+                uint32_t pos;
                 const uint32_t c = pair_count<K, OffT, PEnt, PE, POW2>(kp, cur, soff, i, qn, tb, vb, seed,
-                                                                        hk, nv, compared, key, b, e);
+                                                                        hk, nv, compared, key, b, e, pos);
                 const uint32_t cw = warp_sum(c);
                 if (ch < kPairRound) {
                     if (lane == 0) s_wt[ch * nwarps + warp] = cw;
-                    s_info[ch * kPartProbeBlock + i0] = pair_info(kp, key, b, e, c);
+                    s_info[ch * kPartProbeBlock + i0] = pair_info(b, e, c, pos);
                 }
                 mine += cw;
             }
@@ -750,11 +748,12 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
                         uint64_t b, e, dummy = 0;
                         const uint64_t i = ch * kPartProbeBlock + warp * 32 + lane;
                         const PEnt cur = i < qn ? ep[i] : PEnt{};
+                        uint32_t pos;
                         const uint32_t c = pair_count<K, OffT, PEnt, PE, POW2>(
-                            kp, cur, soff, i, qn, tb, vb, seed, hk, nv, dummy, key, b, e);
+                            kp, cur, soff, i, qn, tb, vb, seed, hk, nv, dummy, key, b, e, pos);
                         const uint32_t cw = warp_sum(c);
                         if (lane == 0) s_wt[(ch - r0) * nwarps + warp] = cw;
-                        s_info[(ch - r0) * kPartProbeBlock + warp * 32 + lane] = pair_info(kp, key, b, e, c);
+                        s_info[(ch - r0) * kPartProbeBlock + warp * 32 + lane] = pair_info(b, e, c, pos);
                     }
                 }
                 __syncthreads();
@@ -791,8 +790,9 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
                     key = 0;
                     if (__any_sync(0xffffffffu, walk)) {
                         // duplicates / long segments: count again (warp-collective)
+                        uint32_t pos;
                         const uint32_t cc = pair_count<K, OffT, PEnt, PE, POW2>(
-                            kp, cur, soff, i, qn, tb, vb, seed, hk, nv, dummy, key, b, e);
+                            kp, cur, soff, i, qn, tb, vb, seed, hk, nv, dummy, key, b, e, pos);
                         if (walk) c = cc;
                     }
                     if (!walk) b = e = 0;
