@@ -37,9 +37,13 @@ __device__ __forceinline__ T warp_inclusive_sum(T x) {
 
 template <typename T>
 __device__ __forceinline__ T warp_sum(T x) {
+    if constexpr (sizeof(T) == 4) {
+        return T(__reduce_add_sync(0xffffffffu, uint32_t(x)));  // one REDUX (sm_80+)
+    } else {
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
-    return x;
+        for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
+        return x;
+    }
 }
 
 // Loads kScanItems consecutive elements of `in` starting at element `base`
