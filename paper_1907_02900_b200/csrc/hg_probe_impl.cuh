@@ -24,6 +24,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cmath>
 
 #include "hg_common.cuh"
 #include "hg_internal.h"
@@ -597,6 +598,12 @@ __device__ __forceinline__ uint32_t pair_count(const K* __restrict__ kp, const P
 
 constexpr uint32_t kNeedWalk = 0xFFFFFFFFu;
 
+// Shared bytes of the single-pass pairs kernel's staged table-value slice.
+template <typename VT>
+__host__ __device__ constexpr size_t pair_val_bytes(uint32_t kcap) {
+    return (size_t(kcap) * sizeof(VT) + 32 + 15) & ~size_t(15);
+}
+
 // Pass-A summary of one probe for pass B: 0 (no match), (t << 16) | 1 (one
 // match at tile key t = b + pos, short segment, t < 2^16) or kNeedWalk.
 __device__ __forceinline__ uint32_t pair_info(uint64_t b, uint64_t e, uint32_t c, uint32_t pos) {
@@ -622,12 +629,16 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
     unsigned char* const b_off = smem;
     unsigned char* const b_key = smem + L::off_bytes(P);
     unsigned char* const b_ent = b_key + L::key_bytes(kcap);
+    // the partition's table values (build entry indices of the pairs) are
+    // staged next to its keys: the pair writes read them from shared memory
+    // instead of one random L2 gather per pair
+    unsigned char* const b_val = b_ent + L::ent_bytes(pcap);
     // per-probe result of pass A for the current round: 0 = no match,
     // (t << 16) | 1 = exactly one match at tile key t, kNeedWalk = walk again
-    uint32_t* const s_info = reinterpret_cast<uint32_t*>(b_ent + L::ent_bytes(pcap));
+    uint32_t* const s_info = reinterpret_cast<uint32_t*>(b_val + pair_val_bytes<VT>(kcap));
     __shared__ uint64_t s_bar;
     __shared__ uint64_t s_p, s_tb, s_q0, s_q1, s_base;
-    __shared__ uint32_t s_o0, s_o1, s_o2, s_kst, s_pst;
+    __shared__ uint32_t s_o0, s_o1, s_o2, s_o3, s_kst, s_pst;
     __shared__ uint64_t s_wt[kPairRound * nwarps];
     __shared__ uint64_t s_red[nwarps];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -660,17 +671,21 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
                     lo_off = uint32_t(a - lo);
                     return uint32_t(hi - lo);
                 };
-                uint32_t o0, o1 = 0, o2 = 0;
+                const uintptr_t av = reinterpret_cast<uintptr_t>(tvals + tb);
+                uint32_t o0, o1 = 0, o2 = 0, o3 = 0;
                 const uint32_t l0 = span(ao, size_t(pv + 1) * sizeof(OffT), o0);
                 const uint32_t l1 = s_kst ? span(ak, size_t(te - tb) * sizeof(K), o1) : 0;
                 const uint32_t l2 = s_pst ? span(ae, size_t(q1 - q0) * sizeof(PEnt), o2) : 0;
+                const uint32_t l3 = s_kst ? span(av, size_t(te - tb) * sizeof(VT), o3) : 0;
                 s_o0 = o0;
                 s_o1 = o1;
                 s_o2 = o2;
-                mbar_arrive_expect_tx(&s_bar, l0 + l1 + l2);
+                s_o3 = o3;
+                mbar_arrive_expect_tx(&s_bar, l0 + l1 + l2 + l3);
                 tma_load_1d(b_off, reinterpret_cast<const void*>(ao - o0), l0, &s_bar);
                 if (l1) tma_load_1d(b_key, reinterpret_cast<const void*>(ak - o1), l1, &s_bar);
                 if (l2) tma_load_1d(b_ent, reinterpret_cast<const void*>(ae - o2), l2, &s_bar);
+                if (l3) tma_load_1d(b_val, reinterpret_cast<const void*>(av - o3), l3, &s_bar);
             }
         }
         __syncthreads();
@@ -683,6 +698,8 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
         mbar_wait(&s_bar, phase);
         phase ^= 1;
         const uint64_t nchunks = (qn + kPartProbeBlock - 1) / kPartProbeBlock;
+        const VT* __restrict__ vp =
+            s_kst ? reinterpret_cast<const VT*>(b_val + s_o3) : tvals + tb;  // partition's values
         auto run = [&](const K* __restrict__ kp, const PEnt* __restrict__ ep) {
             // A: counts; (chunk, warp) totals of the first round
             uint64_t mine = 0;
@@ -802,11 +819,11 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
                     const uint64_t pidx = PE::kHasVal && i < qn ? uint64_t(PE::val(cur)) : 0;
                     if (!walk && c == 1) {
                         // one match at a known tile key: one value gather + store
-                        if (sl < cap) store_pair<PT>(pairs, sl, uint64_t(tvals[tb + (info >> 16)]), pidx);
+                        if (sl < cap) store_pair<PT>(pairs, sl, uint64_t(vp[info >> 16]), pidx);
                     } else if (c && len <= kLongSeg) {
                         for (uint64_t t = b; t < e && sl < cap; ++t) {
                             if (kp[t] == key) {
-                                store_pair<PT>(pairs, sl, uint64_t(tvals[tb + t]), pidx);
+                                store_pair<PT>(pairs, sl, uint64_t(vp[t]), pidx);
                                 ++sl;
                             }
                         }
@@ -825,7 +842,7 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
                             const bool hit = t < ke && kp[t] == kk;
                             const uint32_t hm = __ballot_sync(0xffffffffu, hit);
                             const uint64_t my = ws + __popc(hm & lanemask_lt());
-                            if (hit && my < cap) store_pair<PT>(pairs, my, uint64_t(tvals[tb + t]), pj);
+                            if (hit && my < cap) store_pair<PT>(pairs, my, uint64_t(vp[t]), pj);
                             ws += __popc(hm);
                         }
                     }
@@ -893,6 +910,17 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
             else kcap -= kcap / 4;
         }
         while (E1L::bytes(P, kcap, 0) + round > optin && kcap > 512) kcap -= kcap / 4;
+    }
+    // single-pass pairs kernel: keys AND values of the partition staged, two
+    // CTAs per SM -> a tighter key cap (mean + 6 sigma of a Poisson count)
+    uint32_t kcap_pairs = uint32_t(std::min<double>(kcap, std::max(512.0, kmean + 6.0 * std::sqrt(kmean) + 64)));
+    {
+        using E1L = ProbeLayout<K, OffT, typename EntryT<K, IT>::T>;
+        const size_t optin = smem_optin() - 8192;
+        const size_t round = size_t(kPairRound) * kPartProbeBlock * sizeof(uint32_t);
+        while (E1L::bytes(P, kcap_pairs, 0) + pair_val_bytes<VT>(kcap_pairs) + round > optin &&
+               kcap_pairs > 512)
+            kcap_pairs -= kcap_pairs / 4;
     }
     const int sms = num_sms();
     cudaError_t e;
@@ -986,7 +1014,8 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
         // the pairs kernel reads its probe entries straight from global memory
         // (coalesced; its second pass hits L2), so only the offsets and table
         // keys are staged and more CTAs fit per SM
-        const size_t smem_pairs = ProbeLayout<K, OffT, E1>::bytes(P, kcap, 0) +
+        const size_t smem_pairs = ProbeLayout<K, OffT, E1>::bytes(P, kcap_pairs, 0) +
+                                  pair_val_bytes<VT>(kcap_pairs) +
                                   size_t(kPairRound) * kPartProbeBlock * sizeof(uint32_t);
         auto launch_pairs = [&](auto kern, uint64_t* status) -> cudaError_t {
             const size_t smem = smem_pairs;
@@ -1001,7 +1030,7 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
             HG_LAUNCH("k10p_probe_pairs", s,
                       kern<<<gk, kPartProbeBlock, smem, s>>>(
                           static_cast<const E1*>(reorg), ppart, g.nparts, t.nv, t.seed,
-                          t.hash_kind, nv, g.pshift, offs, tkeys, tvals, kcap, 0, status,
+                          t.hash_kind, nv, g.pshift, offs, tkeys, tvals, kcap_pairs, 0, status,
                           a.pairs, a.cap, a.totals, ticket));
             return cudaGetLastError();
         };
