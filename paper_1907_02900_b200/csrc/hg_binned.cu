@@ -47,7 +47,7 @@ static const char* const kBuildPassNames[3] = {"k4_part_hist", "k6a_multisplit",
 template <typename K, typename VT>
 struct BuildLayout {
     using E = typename EntryT<K, VT>::T;
-    static constexpr int kItems = sizeof(E) >= 16 ? 6 : 9;
+    static constexpr int kItems = sizeof(E) >= 16 ? 6 : 11;
     static constexpr uint32_t kCap = kBuildBlock * kItems;  // staged entries per partition
     __host__ __device__ static size_t in_bytes() { return align16(size_t(kCap) * sizeof(E) + 32); }
     __host__ __device__ static size_t k_bytes() { return align16(size_t(kCap + 4) * sizeof(K)); }
