@@ -292,22 +292,63 @@ __device__ __forceinline__ uint32_t big_owner(const uint64_t* pref, uint32_t nb,
     return lo;
 }
 
+// Exclusive prefixes of the queued partitions' entry counts (pref) and K7b
+// chunk counts (cpref), one CTA: each thread sums a run of consecutive list
+// entries, a block scan of the run totals, then the runs are written
+// (round 1 walked the list with one thread: 65536 dependent loads for C3).
+constexpr int kBigPrefixBlock = 1024;
+
 template <typename OffT>
-__global__ void k7b_prefix(const OffT* __restrict__ part_start, const uint32_t* __restrict__ list,
-                           const uint32_t* __restrict__ big_n, uint64_t* __restrict__ pref,
-                           uint64_t* __restrict__ cpref) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__global__ void __launch_bounds__(kBigPrefixBlock)
+k7b_prefix(const OffT* __restrict__ part_start, const uint32_t* __restrict__ list,
+           const uint32_t* __restrict__ big_n, uint64_t* __restrict__ pref,
+           uint64_t* __restrict__ cpref) {
+    __shared__ uint64_t s_a[kBigPrefixBlock / 32], s_c[kBigPrefixBlock / 32];
     const uint32_t nb = *big_n;
-    uint64_t acc = 0, cacc = 0;
-    for (uint32_t i = 0; i < nb; ++i) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t per = (nb + kBigPrefixBlock - 1) / kBigPrefixBlock;
+    const uint32_t i0 = min(nb, tid * per), i1 = min(nb, i0 + per);
+    auto size_of = [&](uint32_t i) {
+        return uint64_t(part_start[list[i] + 1]) - uint64_t(part_start[list[i]]);
+    };
+    uint64_t a = 0, c = 0;
+    for (uint32_t i = i0; i < i1; ++i) {
+        const uint64_t sz = size_of(i);
+        a += sz;
+        c += (sz + kBigChunk - 1) / kBigChunk;
+    }
+    uint64_t ia = a, ic = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t ya = __shfl_up_sync(0xffffffffu, ia, d);
+        const uint64_t yc = __shfl_up_sync(0xffffffffu, ic, d);
+        if (int(lane) >= d) {
+            ia += ya;
+            ic += yc;
+        }
+    }
+    if (lane == 31) {
+        s_a[warp] = ia;
+        s_c[warp] = ic;
+    }
+    __syncthreads();
+    uint64_t ba = 0, bc = 0;
+    for (uint32_t w = 0; w < warp; ++w) {
+        ba += s_a[w];
+        bc += s_c[w];
+    }
+    uint64_t acc = ba + ia - a, cacc = bc + ic - c;
+    for (uint32_t i = i0; i < i1; ++i) {
         pref[i] = acc;
         cpref[i] = cacc;
-        const uint64_t sz = uint64_t(part_start[list[i] + 1]) - uint64_t(part_start[list[i]]);
+        const uint64_t sz = size_of(i);
         acc += sz;
         cacc += (sz + kBigChunk - 1) / kBigChunk;
     }
-    pref[nb] = acc;
-    cpref[nb] = cacc;
+    if (tid == kBigPrefixBlock - 1) {
+        pref[nb] = ba + ia;
+        cpref[nb] = bc + ic;
+    }
 }
 
 // Block-aggregated variant for partitions of <= 2^14 vertices: a CTA takes a
@@ -526,7 +567,9 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
         // when there are none)
         uint32_t* big_n = ticket + 1;
         uint64_t* big_cpref = big_pref + g.nparts + 1;
-        k7b_prefix<OffT><<<1, 32, 0, s>>>(part_start, big_list, big_n, big_pref, big_cpref);
+        HG_LAUNCH("k7b_big_prefix", s,
+                  (k7b_prefix<OffT><<<1, kBigPrefixBlock, 0, s>>>(part_start, big_list, big_n,
+                                                                  big_pref, big_cpref)));
         const unsigned gb = unsigned(num_sms() * 8);
         // block-aggregated K7b when a partition's counters fit shared memory
         const size_t hsm = (size_t(1) << g.pshift) * sizeof(OffT);

@@ -432,18 +432,33 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
 }
 
 // Pass-2 tile layout: tile_prefix[b] = sum over buckets < b of ceil(size/tile).
+// One CTA of kMaxDigits threads: thread b sizes bucket b, then a block scan
+// (round 1 ran this as one thread walking 256 dependent global loads:
+// ~135 us per launch, twice per C2 step).
 template <typename OffT>
-__global__ void k_tile_prefix(const OffT* __restrict__ part_start, uint64_t nparts, uint32_t nb1,
-                              uint32_t b2, uint32_t kSplitTile, uint64_t* __restrict__ tile_prefix) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    uint64_t acc = 0;
-    for (uint32_t b = 0; b < nb1; ++b) {
-        tile_prefix[b] = acc;
+__global__ void __launch_bounds__(kMaxDigits)
+k_tile_prefix(const OffT* __restrict__ part_start, uint64_t nparts, uint32_t nb1, uint32_t b2,
+              uint32_t kSplitTile, uint64_t* __restrict__ tile_prefix) {
+    __shared__ uint64_t s_w[kMaxDigits / 32];
+    const uint32_t b = threadIdx.x, lane = b & 31, warp = b >> 5;
+    uint64_t c = 0;
+    if (b < nb1) {
         const uint64_t hi = (uint64_t(b + 1) << b2) < nparts ? (uint64_t(b + 1) << b2) : nparts;
         const uint64_t sz = uint64_t(part_start[hi]) - uint64_t(part_start[uint64_t(b) << b2]);
-        acc += (sz + kSplitTile - 1) / kSplitTile;
+        c = (sz + kSplitTile - 1) / kSplitTile;
     }
-    tile_prefix[nb1] = acc;
+    uint64_t inc = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, inc, d);
+        if (int(lane) >= d) inc += y;
+    }
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    uint64_t base = 0;
+    for (uint32_t w = 0; w < warp; ++w) base += s_w[w];
+    if (b < nb1) tile_prefix[b] = base + inc - c;
+    if (b == nb1 - 1) tile_prefix[nb1] = base + inc;
 }
 
 template <typename OffT>
@@ -560,7 +575,7 @@ cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, 
                   in1, vals, val_base, n, seed, hk, nv, g.pshift, g.b2, uint32_t((1u << g.b1) - 1), 0,
                   cur1, part_start, 0, nullptr, tiles1, g.nparts, mid)));
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    k_tile_prefix<OffT><<<1, 32, 0, s>>>(part_start, g.nparts, nb1, g.b2, kSplitTile, tile_prefix);
+    k_tile_prefix<OffT><<<1, kMaxDigits, 0, s>>>(part_start, g.nparts, nb1, g.b2, kSplitTile, tile_prefix);
     const uint64_t tiles2 = tiles1 + nb1;  // upper bound; exact count = tile_prefix[nb1]
     HG_LAUNCH(names[2], s,
               (ks2<<<g2, kSplitBlock, sm2, s>>>(
