@@ -44,19 +44,29 @@ __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size
 constexpr int kBuildBlock = 512;
 static const char* const kBuildPassNames[3] = {"k4_part_hist", "k6a_multisplit", "k6b_multisplit"};
 
+// 8-byte entries (u32 key + u32 value): the partition's entries arrive by
+// TMA into an input stage (prefetched during the previous partition). 16-byte
+// entries: no input stage -- each thread loads its entries straight from
+// global memory (16-byte coalesced loads) -- so that 9 entries per thread
+// (cap 4608, C3's u64 partitions at load 1 hold ~4096) still fit two CTAs per
+// SM; round 1 staged them with a cap of 3072, which sent every C3 load-1
+// partition to K7b.
 template <typename K, typename VT>
 struct BuildLayout {
     using E = typename EntryT<K, VT>::T;
-    static constexpr int kItems = sizeof(E) >= 16 ? 6 : 11;
-    static constexpr uint32_t kCap = kBuildBlock * kItems;  // staged entries per partition
-    __host__ __device__ static size_t in_bytes() { return align16(size_t(kCap) * sizeof(E) + 32); }
+    static constexpr bool kStageIn = sizeof(E) < 16;
+    static constexpr int kItems = sizeof(E) >= 16 ? 9 : 11;
+    static constexpr uint32_t kCap = kBuildBlock * kItems;  // entries per partition built here
+    __host__ __device__ static size_t in_bytes() {
+        return kStageIn ? align16(size_t(kCap) * sizeof(E) + 32) : 0;
+    }
     __host__ __device__ static size_t k_bytes() { return align16(size_t(kCap + 4) * sizeof(K)); }
     __host__ __device__ static size_t v_bytes() { return align16(size_t(kCap + 4) * sizeof(VT)); }
     static size_t bytes(uint32_t P) { return align16(size_t(P) * 4) + in_bytes() + k_bytes() + v_bytes(); }
 };
 
 template <typename K, typename VT, typename OffT, int POW2>
-__global__ void __launch_bounds__(kBuildBlock)
+__global__ void __launch_bounds__(kBuildBlock, 2)
 k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
              const OffT* __restrict__ part_start /* nparts + 1 partition offsets */,
              uint64_t nparts, uint64_t nv_total, uint64_t seed, int hk, Divisor nv,
@@ -84,9 +94,11 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
     // thread 0: bounds of the partition after the next one (prefetched)
     uint64_t n_s = 0, n_e = 0;
     auto issue = [&](uint64_t s, uint64_t e) {  // thread 0
-        if (e - s <= cap) {
-            fence_proxy_async();
-            s_ofs = tma_load_span(inb, reorg + s, uint32_t((e - s) * sizeof(E)), &s_bar);
+        if constexpr (L::kStageIn) {
+            if (e - s <= cap) {
+                fence_proxy_async();
+                s_ofs = tma_load_span(inb, reorg + s, uint32_t((e - s) * sizeof(E)), &s_bar);
+            }
         }
     };
     if (tid == 0) {
@@ -118,13 +130,22 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
         }
         E ent[kItems];
         if (staged) {
-            mbar_wait(&s_bar, phase);
-            phase ^= 1;
-            const E* src = reinterpret_cast<const E*>(inb + s_ofs);
+            if constexpr (L::kStageIn) {
+                mbar_wait(&s_bar, phase);
+                phase ^= 1;
+                const E* src = reinterpret_cast<const E*>(inb + s_ofs);
 #pragma unroll
-            for (int k = 0; k < kItems; ++k) {
-                const uint32_t i = tid + k * kBuildBlock;
-                if (i < cntp) ent[k] = src[i];
+                for (int k = 0; k < kItems; ++k) {
+                    const uint32_t i = tid + k * kBuildBlock;
+                    if (i < cntp) ent[k] = src[i];
+                }
+            } else {
+                const E* src = reorg + s;
+#pragma unroll
+                for (int k = 0; k < kItems; ++k) {
+                    const uint32_t i = tid + k * kBuildBlock;
+                    if (i < cntp) ent[k] = __ldcs(src + i);
+                }
             }
         }
         __syncthreads();  // cnt zeroed, input buffer consumed
