@@ -56,6 +56,9 @@ struct BuildLayout {
     using E = typename EntryT<K, VT>::T;
     static constexpr bool kStageIn = sizeof(E) < 16;
     static constexpr int kItems = sizeof(E) >= 16 ? 9 : 11;
+    // items past kBase are touched only by partitions larger than kBase * 512
+    // (a warp-uniform branch), so the common case pays for kBase items
+    static constexpr int kBase = sizeof(E) >= 16 ? 9 : 9;
     static constexpr uint32_t kCap = kBuildBlock * kItems;  // entries per partition built here
     __host__ __device__ static size_t in_bytes() {
         return kStageIn ? align16(size_t(kCap) * sizeof(E) + 32) : 0;
@@ -128,24 +131,31 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
         } else {
             for (uint32_t j = tid; j < pv; j += kBuildBlock) cnt[j] = 0;
         }
+        // per-item loops: kBase items unrolled, the rest only for large partitions
+        auto for_items = [&](auto&& f) {
+#pragma unroll
+            for (int k = 0; k < L::kBase; ++k) f(k);
+            if (cntp > uint32_t(L::kBase) * kBuildBlock) {
+#pragma unroll
+                for (int k = L::kBase; k < kItems; ++k) f(k);
+            }
+        };
         E ent[kItems];
         if (staged) {
             if constexpr (L::kStageIn) {
                 mbar_wait(&s_bar, phase);
                 phase ^= 1;
                 const E* src = reinterpret_cast<const E*>(inb + s_ofs);
-#pragma unroll
-                for (int k = 0; k < kItems; ++k) {
+                for_items([&](int k) {
                     const uint32_t i = tid + k * kBuildBlock;
                     if (i < cntp) ent[k] = src[i];
-                }
+                });
             } else {
                 const E* src = reorg + s;
-#pragma unroll
-                for (int k = 0; k < kItems; ++k) {
+                for_items([&](int k) {
                     const uint32_t i = tid + k * kBuildBlock;
                     if (i < cntp) ent[k] = __ldcs(src + i);
-                }
+                });
             }
         }
         __syncthreads();  // cnt zeroed, input buffer consumed
@@ -164,14 +174,13 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
         // (core.hpp:126-133); the returned count is the entry's rank
         uint32_t lr[kItems];
         if (staged) {
-#pragma unroll
-            for (int k = 0; k < kItems; ++k) {
+            for_items([&](int k) {
                 const uint32_t i = tid + k * kBuildBlock;
                 if (i < cntp) {
                     const uint32_t lv = uint32_t(hv<POW2>(PE::key(ent[k]), seed, hk, nv) - vb);
                     lr[k] = (lv << 16) | atomicAdd(cnt + lv, 1u);
                 }
-            }
+            });
         } else {
             // oversized (skewed) partition: built by the grid-wide K7b
             // kernels; here only its counters (offs[vb+1 .. vb+pv]) are zeroed
@@ -263,15 +272,14 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
             // arrays of a vertex-range slice start at any entry)
             K* skp = sk + ((reinterpret_cast<uintptr_t>(okeys + s) / sizeof(K)) & (KA - 1));
             VT* svp = sv + ((reinterpret_cast<uintptr_t>(ovals + s) / sizeof(VT)) & (VA - 1));
-#pragma unroll
-            for (int k = 0; k < kItems; ++k) {
+            for_items([&](int k) {
                 const uint32_t i = tid + k * kBuildBlock;
                 if (i < cntp) {
                     const uint32_t pos = cnt[lr[k] >> 16] + (lr[k] & 0xFFFFu);
                     skp[pos] = PE::key(ent[k]);
                     svp[pos] = PE::val(ent[k]);
                 }
-            }
+            });
             fence_proxy_async();
             __syncthreads();
             const bool a = bulk_store_span(okeys + s, skp, cntp, tid, kBuildBlock);
