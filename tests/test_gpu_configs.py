@@ -271,3 +271,26 @@ def test_sharded_engine_over_nccl_world1(cuda, oracle):
         del st
     finally:
         dist.destroy_process_group()
+
+
+def test_pipelined_host_probes_stream_order(cuda):
+    """pinned host probes written by earlier work on the
+    caller's stream (a pending device->host copy) are copied for the probe
+    only after that work -- the chunked pipeline waits on the stream unless
+    the caller passes host_ready (HG_PROBE_HOST_READY)."""
+    n, m = 1 << 22, (1 << 27) + 4096
+    keys = cuda.empty(n, dtype=cuda.int32, device="cuda")
+    hg.generate(keys, kind=0, seed=1)
+    t = hg.build_v2(keys)
+    probes = cuda.empty(m, dtype=cuda.int32, device="cuda")
+    hg.generate(probes, kind=0, seed=2)
+    probes[: n] = keys  # n hits at least
+    ref = cuda.zeros(2, dtype=cuda.int64, device="cuda")
+    hg.probe_device(t, probes, ref)
+    hp = cuda.zeros(m, dtype=cuda.int32).pin_memory()  # stale contents: all zero
+    s = cuda.cuda.current_stream()
+    cuda.cuda._sleep(50_000_000)                        # keep the stream busy a while
+    hp.copy_(probes, non_blocking=True)                 # pending D2H on the stream
+    r = hg.probe_standard(t, hp)                        # must see the copied probes
+    assert (r.match_count, r.key_comparisons) == tuple(int(x) for x in ref.cpu().tolist())
+    s.synchronize()
