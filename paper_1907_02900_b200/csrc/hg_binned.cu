@@ -74,7 +74,11 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
              const OffT* __restrict__ part_start /* nparts + 1 partition offsets */,
              uint64_t nparts, uint64_t nv_total, uint64_t seed, int hk, Divisor nv,
              uint32_t pshift, uint64_t obase, OffT* __restrict__ offs, K* __restrict__ okeys,
-             VT* __restrict__ ovals, uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_n) {
+             VT* __restrict__ ovals, uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_n,
+             uint64_t in_cap, const uint32_t* __restrict__ slack_flag) {
+    // partition p's input: the slack layout (p * in_cap) of partition_slack
+    // unless it overflowed, else the dense layout (part_start[p])
+    const bool slack_in = in_cap && !*slack_flag;
     using PE = EntryT<K, VT>;
     using E = typename PE::T;
     using L = BuildLayout<K, VT>;
@@ -96,11 +100,12 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
 
     // thread 0: bounds of the partition after the next one (prefetched)
     uint64_t n_s = 0, n_e = 0;
-    auto issue = [&](uint64_t s, uint64_t e) {  // thread 0
+    auto in_of = [&](uint64_t p, uint64_t s) -> uint64_t { return slack_in ? p * in_cap : s; };
+    auto issue = [&](uint64_t p, uint64_t s, uint64_t e) {  // thread 0
         if constexpr (L::kStageIn) {
             if (e - s <= cap) {
                 fence_proxy_async();
-                s_ofs = tma_load_span(inb, reorg + s, uint32_t((e - s) * sizeof(E)), &s_bar);
+                s_ofs = tma_load_span(inb, reorg + in_of(p, s), uint32_t((e - s) * sizeof(E)), &s_bar);
             }
         }
     };
@@ -111,7 +116,7 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
         if (p0 < nparts) {
             s_s = part_start[p0];
             s_e = part_start[p0 + 1];
-            issue(s_s, s_e);
+            issue(p0, s_s, s_e);
         }
         if (p0 + step < nparts) {
             n_s = part_start[p0 + step];
@@ -151,7 +156,7 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
                     if (i < cntp) ent[k] = src[i];
                 });
             } else {
-                const E* src = reorg + s;
+                const E* src = reorg + in_of(p, s);
                 for_items([&](int k) {
                     const uint32_t i = tid + k * kBuildBlock;
                     if (i < cntp) ent[k] = __ldcs(src + i);
@@ -162,7 +167,7 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
         if (tid == 0) {
             // next partition's entries stream in while this one is built
             const uint64_t pn = p + step;
-            if (pn < nparts) issue(n_s, n_e);
+            if (pn < nparts) issue(pn, n_s, n_e);
             s_s = n_s;
             s_e = n_e;
             if (pn + step < nparts) {
@@ -392,7 +397,9 @@ __global__ void __launch_bounds__(512)
 k7b_chunk(const typename EntryT<K, VT>::T* __restrict__ reorg, const OffT* __restrict__ part_start,
           const uint32_t* __restrict__ list, const uint32_t* __restrict__ big_n,
           const uint64_t* __restrict__ cpref, uint64_t nv_total, uint64_t seed, Divisor nv,
-          uint32_t pshift, OffT* __restrict__ offs, K* __restrict__ okeys, VT* __restrict__ ovals) {
+          uint32_t pshift, OffT* __restrict__ offs, K* __restrict__ okeys, VT* __restrict__ ovals,
+          uint64_t in_cap, const uint32_t* __restrict__ slack_flag) {
+    const bool slack_in = in_cap && !*slack_flag;
     using PE = EntryT<K, VT>;
     extern __shared__ __align__(128) unsigned char smem[];
     OffT* const hist = reinterpret_cast<OffT*>(smem);
@@ -405,6 +412,8 @@ k7b_chunk(const typename EntryT<K, VT>::T* __restrict__ reorg, const OffT* __res
         const uint32_t li = big_owner(cpref, nb, c);
         const uint64_t p = list[li];
         const uint64_t s = part_start[p], e = part_start[p + 1];
+        // input view at dense indices (pointer arithmetic in 64-bit indices)
+        const typename PE::T* rin = reorg + (slack_in ? p * in_cap : s);
         const uint64_t c0 = s + (c - cpref[li]) * kBigChunk;
         const uint64_t c1 = e < c0 + kBigChunk ? e : c0 + kBigChunk;
         const uint64_t vb = p << pshift;
@@ -416,7 +425,7 @@ k7b_chunk(const typename EntryT<K, VT>::T* __restrict__ reorg, const OffT* __res
             const bool act = j < c1;
             const uint32_t active = __ballot_sync(0xffffffffu, act);
             if (act) {
-                const uint32_t lv = uint32_t(vhash<POW2>(PE::key(reorg[j]), seed, nv) - vb);
+                const uint32_t lv = uint32_t(vhash<POW2>(PE::key(rin[j - s]), seed, nv) - vb);
                 aggregated_count<true>(hist + lv, active, lv);
             }
         }
@@ -435,7 +444,7 @@ k7b_chunk(const typename EntryT<K, VT>::T* __restrict__ reorg, const OffT* __res
                 const bool act = j < c1;
                 const uint32_t active = __ballot_sync(0xffffffffu, act);
                 if (act) {
-                    const auto en = reorg[j];
+                    const auto en = rin[j - s];
                     const uint32_t lv = uint32_t(vhash<POW2>(PE::key(en), seed, nv) - vb);
                     const uint64_t slot = aggregated_ticket<true>(hist + lv, active, lv);
                     okeys[slot] = PE::key(en);
@@ -453,8 +462,10 @@ __global__ void __launch_bounds__(256)
 k7b_pass(const typename EntryT<K, VT>::T* __restrict__ reorg, const OffT* __restrict__ part_start,
          const uint32_t* __restrict__ list, const uint32_t* __restrict__ big_n,
          const uint64_t* __restrict__ pref, uint64_t seed, Divisor nv, uint32_t pshift,
-         OffT* __restrict__ offs, K* __restrict__ okeys, VT* __restrict__ ovals) {
+         OffT* __restrict__ offs, K* __restrict__ okeys, VT* __restrict__ ovals, uint64_t in_cap,
+         const uint32_t* __restrict__ slack_flag) {
     using PE = EntryT<K, VT>;
+    const bool slack_in = in_cap && !*slack_flag;
     constexpr bool V32 = sizeof(OffT) == 4;
     const uint32_t nb = *big_n;
     if (nb == 0) return;
@@ -467,7 +478,7 @@ k7b_pass(const typename EntryT<K, VT>::T* __restrict__ reorg, const OffT* __rest
         if (!act) continue;
         const uint32_t li = big_owner(pref, nb, g);
         const uint64_t p = list[li];
-        const uint64_t pos = uint64_t(part_start[p]) + (g - pref[li]);
+        const uint64_t pos = (slack_in ? p * in_cap : uint64_t(part_start[p])) + (g - pref[li]);
         const auto en = reorg[pos];
         const uint64_t v = vhash<POW2>(PE::key(en), seed, nv);  // local vertex id
         if constexpr (!PLACE) {
@@ -552,9 +563,14 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
     const PartGeom g = make_geom(t.nv, t.n, a.partition_vertices, sizeof(E) >= 16 ? 2048.0 : 4096.0);
     const size_t smem = BuildLayout<K, VT>::bytes(1u << g.pshift);
 
+    // slack (histogram-free) partition layout when it fits; the flag word
+    // lives in the scratch tail (ticket + 2)
+    const Slack sl_caps = make_slack<OffT>(g, t.n, t.nv, nullptr);
+    const uint64_t nb1 = (g.nparts + (uint64_t(1) << g.b2) - 1) >> g.b2;
     const size_t ps_bytes = ((g.nparts + 1) * sizeof(OffT) + 255) & ~size_t(255);
-    const size_t pscr = PartitionScratch<K, VT, OffT>::bytes(g, t.n);
-    const size_t reorg_bytes = (t.n * sizeof(E) + 255) & ~size_t(255);
+    const size_t pscr = PartitionScratch<K, VT, OffT>::bytes(g, t.n, nb1 * sl_caps.cap1);
+    const uint64_t reorg_n = std::max<uint64_t>(t.n, g.nparts * sl_caps.cap2);
+    const size_t reorg_bytes = (reorg_n * sizeof(E) + 255) & ~size_t(255);
     // K7b queue: at most nparts oversized partitions
     const size_t list_bytes = ((g.nparts + 1) * 4 + 255) & ~size_t(255);
     const size_t pref_bytes = (2 * (g.nparts + 1) * 8 + 255) & ~size_t(255);  // pref | cpref
@@ -569,13 +585,16 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
     uint32_t* big_list = reinterpret_cast<uint32_t*>(scratch + ps_bytes + pscr + reorg_bytes);
     uint64_t* big_pref = reinterpret_cast<uint64_t*>(scratch + ps_bytes + pscr + reorg_bytes + list_bytes);
     uint32_t* ticket = reinterpret_cast<uint32_t*>(scratch + ps_bytes + pscr + reorg_bytes + list_bytes +
-                                                   pref_bytes);  // ticket, big_n
+                                                   pref_bytes);  // ticket, big_n, slack flag
+    Slack sl = sl_caps;
+    sl.flag = ticket + 2;
     do {
-        if ((e = cudaMemsetAsync(ticket, 0, 8, s)) != cudaSuccess) break;  // ticket, big_n
+        if ((e = cudaMemsetAsync(ticket, 0, 16, s)) != cudaSuccess) break;  // ticket, big_n, flag
         e = partition<K, VT, OffT, POW2>(static_cast<const K*>(a.keys),
                                          static_cast<const VT*>(a.vals), t.n, t.seed, t.hash_kind,
                                          nv, g, part_start, pscratch, reorg, s, kBuildPassNames,
-                                         static_cast<const E*>(a.records));
+                                         static_cast<const E*>(a.records), 0, &sl);
+        const uint64_t in_cap = sl.cap1 && sl.cap2 && g.b2 > 0 ? sl.cap2 : 0;
         if (e != cudaSuccess) break;
         auto kb = k_part_build<K, VT, OffT, POW2>;
         if ((e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -590,7 +609,7 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
                                                    t.hash_kind, nv, g.pshift, t.obase, offs,
                                                    static_cast<K*>(t.keys),
                                                    static_cast<VT*>(t.vals), big_list,
-                                                   ticket + 1));
+                                                   ticket + 1, in_cap, sl.flag));
         if ((e = cudaGetLastError()) != cudaSuccess) break;
         // oversized partitions (device-side count; the kernels exit at once
         // when there are none)
@@ -615,7 +634,8 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
             const unsigned gc = unsigned(num_sms() * 3);
             HG_LAUNCH("k7b_big_count", s,
                       (kc0<<<gc, 512, hsm, s>>>(reorg, part_start, big_list, big_n, big_cpref, t.nv,
-                                               t.seed, nv, g.pshift, offs, nullptr, nullptr)));
+                                               t.seed, nv, g.pshift, offs, nullptr, nullptr, in_cap,
+                                               sl.flag)));
             HG_LAUNCH("k7b_big_scan", s,
                       (k7b_scan<OffT><<<unsigned(num_sms() * 2), 1024, 0, s>>>(part_start, big_list,
                                                                            big_n, t.nv, g.pshift,
@@ -623,14 +643,14 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
             HG_LAUNCH("k7b_big_place", s,
                       (kc1<<<gc, 512, hsm, s>>>(reorg, part_start, big_list, big_n, big_cpref, t.nv,
                                                t.seed, nv, g.pshift, offs, static_cast<K*>(t.keys) - t.obase,
-                                               static_cast<VT*>(t.vals) - t.obase)));
+                                               static_cast<VT*>(t.vals) - t.obase, in_cap, sl.flag)));
             e = cudaGetLastError();
             break;
         }
         HG_LAUNCH("k7b_big_count", s,
                   (k7b_pass<K, VT, OffT, POW2, false><<<gb, 256, 0, s>>>(
                       reorg, part_start, big_list, big_n, big_pref, t.seed, nv, g.pshift, offs,
-                      nullptr, nullptr)));
+                      nullptr, nullptr, in_cap, sl.flag)));
         HG_LAUNCH("k7b_big_scan", s,
                   (k7b_scan<OffT><<<unsigned(num_sms() * 2), 1024, 0, s>>>(part_start, big_list,
                                                                        big_n, t.nv, g.pshift,
@@ -638,7 +658,8 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
         HG_LAUNCH("k7b_big_place", s,
                   (k7b_pass<K, VT, OffT, POW2, true><<<gb, 256, 0, s>>>(
                       reorg, part_start, big_list, big_n, big_pref, t.seed, nv, g.pshift, offs,
-                      static_cast<K*>(t.keys) - t.obase, static_cast<VT*>(t.vals) - t.obase)));
+                      static_cast<K*>(t.keys) - t.obase, static_cast<VT*>(t.vals) - t.obase, in_cap,
+                      sl.flag)));
         e = cudaGetLastError();
     } while (false);
     cudaFreeAsync(scratch, s);

@@ -337,7 +337,11 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
              const VT* __restrict__ tvals, uint32_t kcap, uint32_t pcap,
              uint32_t* __restrict__ pcount, const uint64_t* __restrict__ pair_off,
              void* __restrict__ pairs, uint64_t cap, uint64_t* __restrict__ totals,
-             uint32_t* ticket, HeavyQueue heavy) {
+             uint32_t* ticket, HeavyQueue heavy, uint64_t in_cap,
+             const uint32_t* __restrict__ slack_flag) {
+    // probe entries of partition p: slack layout (p * in_cap) of
+    // partition_slack unless it overflowed, else dense (ppart[p])
+    const bool slack_in = in_cap && !*slack_flag;
     using PE = EntryT<K, IT>;
     using PEnt = typename PE::T;
     using L = ProbeLayout<K, OffT, PEnt>;
@@ -347,7 +351,7 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
     unsigned char* const b_key = smem + L::off_bytes(P);
     unsigned char* const b_ent = b_key + L::key_bytes(kcap);
     __shared__ uint64_t s_bar;
-    __shared__ uint64_t s_p, s_tb, s_te, s_q0, s_q1;
+    __shared__ uint64_t s_p, s_tb, s_te, s_q0, s_q1, s_qin;
     __shared__ uint32_t s_o0, s_o1, s_o2, s_kst, s_pst;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr uint32_t nwarps = kPartProbeBlock / 32;
@@ -366,14 +370,15 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
                 const uint32_t pv = uint32_t(nv_total - vb < P ? nv_total - vb : uint64_t(P));
                 const uint64_t tb = offs[vb], te = offs[vb + pv];
                 const uint64_t q0 = ppart[p], q1 = ppart[p + 1];
-                s_tb = tb; s_te = te; s_q0 = q0; s_q1 = q1;
+                const uint64_t qin = slack_in ? p * in_cap : q0;
+                s_tb = tb; s_te = te; s_q0 = q0; s_q1 = q1; s_qin = qin;
                 s_kst = te - tb <= kcap;
                 s_pst = q1 - q0 <= pcap;
                 fence_proxy_async();
                 // three spans, one transaction barrier
                 const uintptr_t ao = reinterpret_cast<uintptr_t>(offs + vb);
                 const uintptr_t ak = reinterpret_cast<uintptr_t>(tkeys + tb);
-                const uintptr_t ae = reinterpret_cast<uintptr_t>(pin + q0);
+                const uintptr_t ae = reinterpret_cast<uintptr_t>(pin + qin);
                 auto span = [](uintptr_t a, size_t bytes, uint32_t& lo_off) -> uint32_t {
                     const uintptr_t lo = a & ~uintptr_t(15), hi = (a + bytes + 15) & ~uintptr_t(15);
                     lo_off = uint32_t(a - lo);
@@ -517,7 +522,7 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
             run(reinterpret_cast<const K*>(b_key + s_o1), reinterpret_cast<const PEnt*>(b_ent + s_o2));
         } else {
             run(s_kst ? reinterpret_cast<const K*>(b_key + s_o1) : tkeys + tb,
-                s_pst ? reinterpret_cast<const PEnt*>(b_ent + s_o2) : pin + q0);
+                s_pst ? reinterpret_cast<const PEnt*>(b_ent + s_o2) : pin + s_qin);
         }
         __syncthreads();
     }
@@ -929,9 +934,14 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
     using E1 = typename EntryT<K, IT>::T;
     using E0 = typename EntryT<K, void>::T;
     const size_t ent = need_idx ? sizeof(E1) : sizeof(E0);
+    // count-only probes: slack (histogram-free) partition layout when it fits
+    // (partition_slack in hg_radix.cuh; the flag word is ticket + 2)
+    const Slack sl_caps = need_idx ? Slack{} : make_slack<OffT>(g, a.m, t.nv, nullptr);
+    const uint64_t nb1 = (g.nparts + (uint64_t(1) << g.b2) - 1) >> g.b2;
     const size_t pscr = need_idx ? PartitionScratch<K, IT, OffT>::bytes(g, a.m)
-                                 : PartitionScratch<K, void, OffT>::bytes(g, a.m);
-    const size_t reorg_bytes = (a.m * ent + 255) & ~size_t(255);
+                                 : PartitionScratch<K, void, OffT>::bytes(g, a.m, nb1 * sl_caps.cap1);
+    const size_t reorg_bytes =
+        (std::max<uint64_t>(a.m, g.nparts * sl_caps.cap2) * ent + 255) & ~size_t(255);
     const bool single = a.pairs && !want_counts && a.cap > 0;  // k_probe_pairs
     const size_t cnt_bytes = (a.pairs && !single) ? ((a.m * 4 + 255) & ~size_t(255)) : 0;
     const size_t po_bytes = single ? ((g.nparts * 8 + 255) & ~size_t(255))
@@ -965,8 +975,11 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
         cur += heavy_bytes;
         hq.cap = hcap;
     }
-    uint32_t* ticket = reinterpret_cast<uint32_t*>(cur);  // ticket, heavy count
+    uint32_t* ticket = reinterpret_cast<uint32_t*>(cur);  // ticket, heavy count, slack flag
     if (use_heavy) hq.n = ticket + 1;
+    Slack sl = sl_caps;
+    sl.flag = ticket + 2;
+    const uint64_t in_cap = sl.cap1 && sl.cap2 && g.b2 > 0 ? sl.cap2 : 0;
     // deferred heavy walks, after the partitioned kernel (per-probe counts: COUNTS)
     auto run_heavy = [&](bool counts) -> cudaError_t {
         const unsigned gh = unsigned(num_sms() * 2);
@@ -988,9 +1001,11 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
                                              static_cast<E1*>(reorg), s, kProbePassNames,
                                              static_cast<const E1*>(a.records));
         } else {
+            if ((e = cudaMemsetAsync(ticket, 0, 16, s)) != cudaSuccess) break;
             e = partition<K, void, OffT, POW2>(probes, static_cast<const void*>(nullptr), a.m,
                                                t.seed, t.hash_kind, nv, g, ppart, pscratch,
-                                               static_cast<E0*>(reorg), s, kProbePassNames);
+                                               static_cast<E0*>(reorg), s, kProbePassNames, nullptr,
+                                               0, &sl);
         }
         if (e != cudaSuccess) break;
         const size_t smem = ProbeLayout<K, OffT, E1>::bytes(P, kcap, pcap);
@@ -1008,7 +1023,8 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
                       kern<<<gk, kPartProbeBlock, smem, s>>>(
                           static_cast<const E1*>(reorg), ppart, g.nparts, t.nv, t.seed,
                           t.hash_kind, nv, g.pshift, offs, tkeys, tvals, kcap, pcap, pc, po, pr,
-                          cap, a.totals, ticket, (pc == a.counts && pc) ? hq : HeavyQueue{}));
+                          cap, a.totals, ticket, (pc == a.counts && pc) ? hq : HeavyQueue{}, 0,
+                          ticket + 2));
             return cudaGetLastError();
         };
         // the pairs kernel reads its probe entries straight from global memory
@@ -1045,12 +1061,12 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPartProbeBlock, smem0);
             const unsigned gk = unsigned(
                 std::min<uint64_t>(uint64_t(std::max(1, per_sm)) * sms, g.nparts));
-            if ((e = cudaMemsetAsync(ticket, 0, 8, s)) != cudaSuccess) break;
+            if ((e = cudaMemsetAsync(ticket, 0, 8, s)) != cudaSuccess) break;  // not the flag
             HG_LAUNCH("k8p_probe_part", s,
                       kern<<<gk, kPartProbeBlock, smem0, s>>>(
                           static_cast<const E0*>(reorg), ppart, g.nparts, t.nv, t.seed,
                           t.hash_kind, nv, g.pshift, offs, tkeys, tvals, kcap, pcap, nullptr,
-                          nullptr, nullptr, 0, a.totals, ticket, hq));
+                          nullptr, nullptr, 0, a.totals, ticket, hq, in_cap, sl.flag));
             if ((e = cudaGetLastError()) != cudaSuccess) break;
             e = run_heavy(false);
             break;

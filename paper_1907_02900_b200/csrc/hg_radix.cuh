@@ -25,6 +25,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cmath>
 #include <type_traits>
 
 #include "hg_common.cuh"
@@ -130,7 +131,8 @@ __device__ __forceinline__ K key_of(const In& x) {
 template <typename K, typename OffT, int POW2, typename In = K>
 __global__ void __launch_bounds__(kHistBlock)
 k_part_hist(const In* __restrict__ keys, uint64_t n, uint64_t seed, int hk, Divisor nv,
-            uint32_t pshift, uint32_t nparts, OffT* __restrict__ hist) {
+            uint32_t pshift, uint32_t nparts, OffT* __restrict__ hist, const uint32_t* guard) {
+    if (guard && !*guard) return;
     extern __shared__ uint32_t sh[];  // nparts/2 words, two 16-bit counters each
     const uint32_t words = (nparts + 1) >> 1;
     for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) sh[i] = 0;
@@ -247,7 +249,15 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
              int hk, Divisor nv, uint32_t pshift, uint32_t dshift, uint32_t dmask, uint32_t b2,
              OffT* __restrict__ cursor, const OffT* __restrict__ part_start, uint32_t nb1,
              const uint64_t* __restrict__ tile_prefix, uint64_t ntiles, uint64_t nparts,
-             typename EntryT<K, VT>::T* __restrict__ out) {
+             typename EntryT<K, VT>::T* __restrict__ out, const uint32_t* guard, uint64_t out_cap,
+             uint32_t* overflow, const OffT* __restrict__ in_end, uint64_t in_cap) {
+    // guard: device-side skip (exact fallback of partition_slack).
+    // out_cap > 0: digit region r = cbase + d of `out` starts at r * out_cap
+    //   and holds out_cap entries; a run that would cross its end sets
+    //   *overflow (the caller falls back to the exact path) and is written,
+    //   in bounds, over the region's end instead.
+    // in_end != nullptr (PASS2): input bucket b is [b * in_cap, in_end[b]).
+    if (guard && !*guard) return;
     using ET = EntryT<K, VT>;
     using E = typename ET::T;
     using L = SplitLayout<K, VT, RAW>;
@@ -273,11 +283,17 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t ndig = dmask + 1;
 
+    // (no static bucket-end cache: p6b's shared memory must stay within two
+    // CTAs per SM; the slack layout's bucket end is read per tile instead)
     if constexpr (PASS2) {
         for (uint32_t b = tid; b <= nb1; b += kSplitBlock) {
             s_tp[b] = tile_prefix[b];
-            const uint64_t q = (uint64_t(b) << b2) < nparts ? (uint64_t(b) << b2) : nparts;
-            s_bs[b] = part_start[q];
+            if (in_end) {
+                s_bs[b] = uint64_t(b) * in_cap;
+            } else {
+                const uint64_t q = (uint64_t(b) << b2) < nparts ? (uint64_t(b) << b2) : nparts;
+                s_bs[b] = part_start[q];
+            }
         }
         __syncthreads();
     }
@@ -291,7 +307,12 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
                 if (s_tp[mid] <= tile) lo = mid; else hi = mid;
             }
             t0 = s_bs[lo] + (tile - s_tp[lo]) * kTile;
-            t1 = s_bs[lo + 1] < t0 + kTile ? s_bs[lo + 1] : t0 + kTile;
+            uint64_t be = s_bs[lo + 1];
+            if (in_end) {
+                const uint64_t e = uint64_t(in_end[lo]);
+                be = e < s_bs[lo] + in_cap ? e : s_bs[lo] + in_cap;
+            }
+            t1 = be < t0 + kTile ? be : t0 + kTile;
             cbase = uint64_t(lo) << b2;
         } else {
             if (tile >= ntiles) return false;
@@ -381,7 +402,16 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
             s_off[tid] = off;
             // the run reservation is consumed only after the scatter below, so
             // its L2 round trip overlaps the scatter
-            if (c) gb = atom_add(cursor + cbase + tid, OffT(c));
+            if (c) {
+                gb = atom_add(cursor + cbase + tid, OffT(c));
+                if (out_cap) {
+                    const uint64_t lim = (cbase + tid + 1) * out_cap;
+                    if (uint64_t(gb) + c > lim) {  // slack region full: exact fallback
+                        *overflow = 1u;
+                        gb = OffT(lim >= c ? lim - c : 0);
+                    }
+                }
+            }
             // digit of every slot of this digit's run, written by the digit's
             // owner as a byte run (word stores in the middle) instead of one
             // random byte store per entry in the scatter; runs longer than
@@ -438,13 +468,22 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
 template <typename OffT>
 __global__ void __launch_bounds__(kMaxDigits)
 k_tile_prefix(const OffT* __restrict__ part_start, uint64_t nparts, uint32_t nb1, uint32_t b2,
-              uint32_t kSplitTile, uint64_t* __restrict__ tile_prefix) {
+              uint32_t kSplitTile, uint64_t* __restrict__ tile_prefix, const uint32_t* guard,
+              const OffT* __restrict__ in_end, uint64_t in_cap) {
+    // in_end != nullptr: bucket b holds in_end[b] - b * in_cap entries (slack layout)
+    if (guard && !*guard) return;
     __shared__ uint64_t s_w[kMaxDigits / 32];
     const uint32_t b = threadIdx.x, lane = b & 31, warp = b >> 5;
     uint64_t c = 0;
     if (b < nb1) {
-        const uint64_t hi = (uint64_t(b + 1) << b2) < nparts ? (uint64_t(b + 1) << b2) : nparts;
-        const uint64_t sz = uint64_t(part_start[hi]) - uint64_t(part_start[uint64_t(b) << b2]);
+        uint64_t sz;
+        if (in_end) {
+            const uint64_t lo = uint64_t(b) * in_cap, e = uint64_t(in_end[b]);
+            sz = (e < lo + in_cap ? e : lo + in_cap) - lo;
+        } else {
+            const uint64_t hi = (uint64_t(b + 1) << b2) < nparts ? (uint64_t(b + 1) << b2) : nparts;
+            sz = uint64_t(part_start[hi]) - uint64_t(part_start[uint64_t(b) << b2]);
+        }
         c = (sz + kSplitTile - 1) / kSplitTile;
     }
     uint64_t inc = c;
@@ -463,12 +502,35 @@ k_tile_prefix(const OffT* __restrict__ part_start, uint64_t nparts, uint32_t nb1
 
 template <typename OffT>
 __global__ void k_init_cursors(const OffT* __restrict__ part_start, uint64_t nparts, uint32_t b2,
-                               uint32_t nb1, OffT* __restrict__ cur1, OffT* __restrict__ cur2) {
+                               uint32_t nb1, OffT* __restrict__ cur1, OffT* __restrict__ cur2,
+                               const uint32_t* guard) {
+    if (guard && !*guard) return;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < nparts; p += stride) {
         cur2[p] = part_start[p];
         if ((p & ((uint64_t(1) << b2) - 1)) == 0 && (p >> b2) < nb1) cur1[p >> b2] = part_start[p];
     }
+}
+
+// Slack layout (partition_slack): pass-1 bucket b at b * cap1, partition p at
+// p * cap2.
+template <typename OffT>
+__global__ void k_init_cursors_slack(uint64_t nparts, uint32_t b2, uint32_t nb1, uint64_t cap1,
+                                     uint64_t cap2, OffT* __restrict__ cur1, OffT* __restrict__ cur2) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < nparts; p += stride) {
+        cur2[p] = OffT(p * cap2);
+        if ((p & ((uint64_t(1) << b2) - 1)) == 0 && (p >> b2) < nb1) cur1[p >> b2] = OffT((p >> b2) * cap1);
+    }
+}
+
+// Partition counts of the slack layout (cursor - region start) -> hist.
+template <typename OffT>
+__global__ void k_slack_counts(const OffT* __restrict__ cur2, uint64_t nparts, uint64_t cap2,
+                               OffT* __restrict__ counts) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < nparts; p += stride)
+        counts[p] = OffT(uint64_t(cur2[p]) - p * cap2);
 }
 
 // Scratch for partition(): histogram, cursors, tile prefix, scan status and
@@ -477,10 +539,11 @@ template <typename K, typename VT, typename OffT>
 struct PartitionScratch {
     using E = typename EntryT<K, VT>::T;
     static size_t up(size_t x) { return (x + 255) / 256 * 256; }
-    static size_t bytes(const PartGeom& g, uint64_t n) {
+    // mid_entries: pass-1 output capacity (slack layout), at least n
+    static size_t bytes(const PartGeom& g, uint64_t n, uint64_t mid_entries = 0) {
         return up((g.nparts + 1) * sizeof(OffT)) * 2 + up(((uint64_t(1) << g.b1) + 1) * sizeof(OffT)) +
                up(((uint64_t(1) << g.b1) + 2) * 8) + up(scan_scratch_bytes(g.nparts)) +
-               (g.b2 ? up(n * sizeof(E)) : 0);
+               (g.b2 ? up((mid_entries > n ? mid_entries : n) * sizeof(E)) : 0);
     }
 };
 
@@ -488,11 +551,50 @@ struct PartitionScratch {
 // out[part_start[p] .. part_start[p+1]) holds the entries of partition p
 // (p = h(key) >> pshift). part_start (nparts + 1 entries, device) receives
 // the partition offsets; part_start[nparts] = n.
+// Optimistic ("slack") layout of a two-pass partition: pass-1 bucket b is
+// written to [b * cap1, b * cap1 + count_b) and partition p to
+// [p * cap2, p * cap2 + count_p), capacities ~8 sigma above the mean of a
+// uniform hash, so no histogram pass is needed; the exact partition starts
+// come from a scan of the final cursors. A region that overflows (skewed
+// keys) sets *flag, and the exact path (histogram, scan, two passes into the
+// dense layout) then runs behind device-side guards -- its kernels exit at
+// once when *flag is 0. Consumers read partition p at
+// (*flag ? part_start[p] : p * cap2), part_start[p + 1] - part_start[p]
+// entries.
+struct Slack {
+    uint64_t cap1 = 0, cap2 = 0;
+    uint32_t* flag = nullptr;  // device, zeroed by the caller
+};
+
+// ~8 sigma of a Poisson count above its mean: the slack capacity of a region
+// expecting `mean` entries.
+inline uint64_t slack_cap(double mean) {
+    return uint64_t(mean + 8.0 * std::sqrt(mean > 1.0 ? mean : 1.0) + 64.0);
+}
+
+// Slack capacities for n entries over geometry g (two passes), or none
+// (cap1 = cap2 = 0) when the slack layout would not fit the offsets' width.
+template <typename OffT>
+inline Slack make_slack(const PartGeom& g, uint64_t n, uint64_t nv, uint32_t* flag) {
+    Slack sl;
+    if (g.b2 == 0 || n < (uint64_t(1) << 20)) return sl;
+    const uint32_t nb1 = uint32_t((g.nparts + (uint64_t(1) << g.b2) - 1) >> g.b2);
+    const double per_vertex = double(n) / double(nv);
+    sl.cap2 = slack_cap(per_vertex * double(uint64_t(1) << g.pshift));
+    sl.cap1 = slack_cap(per_vertex * double(uint64_t(1) << (g.pshift + g.b2)));
+    sl.flag = flag;
+    const uint64_t lim = sizeof(OffT) == 4 ? (uint64_t(1) << 32) - 1 : ~uint64_t(0) >> 2;
+    if (double(nb1) * double(sl.cap1) >= double(lim) || double(g.nparts) * double(sl.cap2) >= double(lim))
+        return Slack{};
+    return sl;
+}
+
 template <typename K, typename VT, typename OffT, int POW2>
 cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, int hk,
                       const Divisor& nv, const PartGeom& g, OffT* part_start, void* scratch,
                       typename EntryT<K, VT>::T* out, cudaStream_t s, const char* const names[3],
-                      const typename EntryT<K, VT>::T* rec = nullptr, uint64_t val_base = 0) {
+                      const typename EntryT<K, VT>::T* rec = nullptr, uint64_t val_base = 0,
+                      const Slack* slack = nullptr) {
     using PS = PartitionScratch<K, VT, OffT>;
     using E = typename EntryT<K, VT>::T;
     char* p = static_cast<char*>(scratch);
@@ -508,41 +610,14 @@ cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, 
     p += PS::up(scan_scratch_bytes(g.nparts));
     E* mid = reinterpret_cast<E*>(p);
 
-    cudaError_t e = cudaMemsetAsync(hist, 0, g.nparts * sizeof(OffT), s);
-    if (e != cudaSuccess) return e;
+    const bool opt = slack && slack->cap1 && slack->cap2 && g.b2 > 0;
+    const uint32_t* guard = opt ? slack->flag : nullptr;
+    cudaError_t e = cudaSuccess;
     const int sms = num_sms();
-    const size_t hsmem = ((g.nparts + 1) / 2) * 4;
-    auto launch_hist = [&](auto kh, const auto* in) -> cudaError_t {
-        cudaError_t r;
-        if (hsmem > 48 * 1024 &&
-            (r = cudaFuncSetAttribute(kh, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hsmem))) !=
-                cudaSuccess)
-            return r;
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kh, kHistBlock, hsmem);
-        unsigned grid = unsigned(std::max(1, per_sm) * sms);
-        grid = unsigned(std::max<uint64_t>(
-            1, std::min<uint64_t>(grid, (n + kHistBlock * 16 - 1) / (kHistBlock * 16))));
-        HG_LAUNCH(names[0], s, kh<<<grid, kHistBlock, hsmem, s>>>(in, n, seed, hk, nv, g.pshift,
-                                                            uint32_t(g.nparts), hist));
-        return cudaGetLastError();
-    };
-    if constexpr (EntryT<K, VT>::kHasVal) {
-        e = rec ? launch_hist(k_part_hist<K, OffT, POW2, E>, rec)
-                : launch_hist(k_part_hist<K, OffT, POW2>, keys);
-    } else {
-        e = launch_hist(k_part_hist<K, OffT, POW2>, keys);
-    }
-    if (e != cudaSuccess) return e;
-    if ((e = launch_scan<OffT, OffT>(hist, part_start, g.nparts, scan_scr, part_start + g.nparts, s,
-                                     "part_scan")) != cudaSuccess)
-        return e;
     const uint32_t nb1 = uint32_t((g.nparts + (uint64_t(1) << g.b2) - 1) >> g.b2);
-    k_init_cursors<OffT><<<unsigned(std::min<uint64_t>((g.nparts + 255) / 256, 1024)), 256, 0, s>>>(
-        part_start, g.nparts, g.b2, nb1, cur1, cur2);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     constexpr int kSplitTile = split_tile<E>();
     const uint64_t tiles1 = (n + kSplitTile - 1) / kSplitTile;
+    const uint64_t tiles2 = tiles1 + nb1;  // upper bound; exact count = tile_prefix[nb1]
     // pass 1 reads the raw keys (+ values), or routed records (entries already)
     auto ks1 = rec ? k_multisplit<K, VT, OffT, false, false, POW2>
                    : k_multisplit<K, VT, OffT, true, false, POW2>;
@@ -562,25 +637,84 @@ cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, 
         1, std::min<uint64_t>(tiles1, uint64_t(sms) * std::max(1, occ1))));
     const unsigned g2 = unsigned(std::max<uint64_t>(
         1, std::min<uint64_t>(tiles1 + 1, uint64_t(sms) * std::max(1, occ2))));
+    const unsigned gi = unsigned(std::min<uint64_t>((g.nparts + 255) / 256, 1024));
+
+    if (opt) {
+        // ---- optimistic: no histogram, slack regions
+        k_init_cursors_slack<OffT><<<gi, 256, 0, s>>>(g.nparts, g.b2, nb1, slack->cap1, slack->cap2,
+                                                      cur1, cur2);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        HG_LAUNCH(names[1], s,
+                  (ks1<<<g1, kSplitBlock, sm1, s>>>(
+                      in1, vals, val_base, n, seed, hk, nv, g.pshift, g.b2,
+                      uint32_t((1u << g.b1) - 1), 0, cur1, part_start, 0, nullptr, tiles1,
+                      g.nparts, mid, nullptr, slack->cap1, slack->flag, nullptr, 0)));
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        k_tile_prefix<OffT><<<1, kMaxDigits, 0, s>>>(part_start, g.nparts, nb1, g.b2, kSplitTile,
+                                                     tile_prefix, nullptr, cur1, slack->cap1);
+        HG_LAUNCH(names[2], s,
+                  (ks2<<<g2, kSplitBlock, sm2, s>>>(
+                      mid, nullptr, 0, n, seed, hk, nv, g.pshift, 0, uint32_t((1u << g.b2) - 1),
+                      g.b2, cur2, part_start, nb1, tile_prefix, tiles2, g.nparts, out, nullptr,
+                      slack->cap2, slack->flag, cur1, slack->cap1)));
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        k_slack_counts<OffT><<<gi, 256, 0, s>>>(cur2, g.nparts, slack->cap2, hist);
+        if ((e = launch_scan<OffT, OffT>(hist, part_start, g.nparts, scan_scr, part_start + g.nparts,
+                                         s, "part_scan")) != cudaSuccess)
+            return e;
+        // ---- exact fallback below: every kernel exits at once unless *flag
+    }
+
+    if ((e = cudaMemsetAsync(hist, 0, g.nparts * sizeof(OffT), s)) != cudaSuccess) return e;
+    const size_t hsmem = ((g.nparts + 1) / 2) * 4;
+    auto launch_hist = [&](auto kh, const auto* in) -> cudaError_t {
+        cudaError_t r;
+        if (hsmem > 48 * 1024 &&
+            (r = cudaFuncSetAttribute(kh, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hsmem))) !=
+                cudaSuccess)
+            return r;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kh, kHistBlock, hsmem);
+        unsigned grid = unsigned(std::max(1, per_sm) * sms);
+        grid = unsigned(std::max<uint64_t>(
+            1, std::min<uint64_t>(grid, (n + kHistBlock * 16 - 1) / (kHistBlock * 16))));
+        HG_LAUNCH(names[0], s, kh<<<grid, kHistBlock, hsmem, s>>>(in, n, seed, hk, nv, g.pshift,
+                                                            uint32_t(g.nparts), hist, guard));
+        return cudaGetLastError();
+    };
+    if constexpr (EntryT<K, VT>::kHasVal) {
+        e = rec ? launch_hist(k_part_hist<K, OffT, POW2, E>, rec)
+                : launch_hist(k_part_hist<K, OffT, POW2>, keys);
+    } else {
+        e = launch_hist(k_part_hist<K, OffT, POW2>, keys);
+    }
+    if (e != cudaSuccess) return e;
+    if ((e = launch_scan<OffT, OffT>(hist, part_start, g.nparts, scan_scr, part_start + g.nparts, s,
+                                     "part_scan", guard)) != cudaSuccess)
+        return e;
+    k_init_cursors<OffT><<<gi, 256, 0, s>>>(part_start, g.nparts, g.b2, nb1, cur1, cur2, guard);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (g.b2 == 0) {
         // single pass straight into partition order
         HG_LAUNCH(names[1], s,
                   (ks1<<<g1, kSplitBlock, sm1, s>>>(
                       in1, vals, val_base, n, seed, hk, nv, g.pshift, 0, uint32_t((1u << g.b1) - 1),
-                      0, cur2, part_start, 0, nullptr, tiles1, g.nparts, out)));
+                      0, cur2, part_start, 0, nullptr, tiles1, g.nparts, out, guard, 0, nullptr,
+                      nullptr, 0)));
         return cudaGetLastError();
     }
     HG_LAUNCH(names[1], s,
               (ks1<<<g1, kSplitBlock, sm1, s>>>(
                   in1, vals, val_base, n, seed, hk, nv, g.pshift, g.b2, uint32_t((1u << g.b1) - 1), 0,
-                  cur1, part_start, 0, nullptr, tiles1, g.nparts, mid)));
+                  cur1, part_start, 0, nullptr, tiles1, g.nparts, mid, guard, 0, nullptr, nullptr, 0)));
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    k_tile_prefix<OffT><<<1, kMaxDigits, 0, s>>>(part_start, g.nparts, nb1, g.b2, kSplitTile, tile_prefix);
-    const uint64_t tiles2 = tiles1 + nb1;  // upper bound; exact count = tile_prefix[nb1]
+    k_tile_prefix<OffT><<<1, kMaxDigits, 0, s>>>(part_start, g.nparts, nb1, g.b2, kSplitTile,
+                                                 tile_prefix, guard, nullptr, 0);
     HG_LAUNCH(names[2], s,
               (ks2<<<g2, kSplitBlock, sm2, s>>>(
                   mid, nullptr, 0, n, seed, hk, nv, g.pshift, 0, uint32_t((1u << g.b2) - 1), g.b2,
-                  cur2, part_start, nb1, tile_prefix, tiles2, g.nparts, out)));
+                  cur2, part_start, nb1, tile_prefix, tiles2, g.nparts, out, guard, 0, nullptr,
+                  nullptr, 0)));
     return cudaGetLastError();
 }
 

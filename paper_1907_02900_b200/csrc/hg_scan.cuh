@@ -110,7 +110,9 @@ __device__ __forceinline__ void scan_store(TO* out, uint64_t n, uint64_t base, c
 // zero on entry.
 template <typename TI, typename TO>
 __global__ void __launch_bounds__(kScanBlock)
-k_scan_lookback(const TI* in, TO* out, uint64_t n, uint64_t* status, uint32_t* ticket, TO* total) {
+k_scan_lookback(const TI* in, TO* out, uint64_t n, uint64_t* status, uint32_t* ticket, TO* total,
+                const uint32_t* guard) {
+    if (guard && !*guard) return;  // device-side skip (the exact fallback of partition_slack)
     __shared__ uint32_t s_tile;
     __shared__ TO s_warp[kScanBlock / 32];
     __shared__ TO s_prefix;
@@ -180,7 +182,7 @@ inline size_t scan_scratch_bytes(uint64_t n) { return (scan_num_tiles(n) + 1) * 
 
 template <typename TI, typename TO>
 cudaError_t launch_scan(const TI* in, TO* out, uint64_t n, void* scratch, TO* total, cudaStream_t s,
-                        const char* name = "scan") {
+                        const char* name = "scan", const uint32_t* guard = nullptr) {
     if (n == 0) {
         if (total) return cudaMemsetAsync(total, 0, sizeof(TO), s);
         return cudaSuccess;
@@ -190,7 +192,8 @@ cudaError_t launch_scan(const TI* in, TO* out, uint64_t n, void* scratch, TO* to
     uint32_t* ticket = reinterpret_cast<uint32_t*>(status + tiles);
     cudaError_t e = cudaMemsetAsync(scratch, 0, scan_scratch_bytes(n), s);
     if (e != cudaSuccess) return e;
-    HG_LAUNCH(name, s, k_scan_lookback<TI, TO><<<unsigned(tiles), kScanBlock, 0, s>>>(in, out, n, status, ticket, total));
+    HG_LAUNCH(name, s, k_scan_lookback<TI, TO><<<unsigned(tiles), kScanBlock, 0, s>>>(in, out, n, status, ticket, total,
+                                                                               guard));
     return cudaGetLastError();
 }
 

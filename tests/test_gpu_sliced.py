@@ -241,3 +241,22 @@ def test_route_records_split_path(cuda, G, V):
         assert (a[np.lexsort(a.T[::-1])] == b[np.lexsort(b.T[::-1])]).all(), f"group {g}"
         assert (np.sort(ko[start:start + c].cpu().numpy()) == np.sort(a[:, 0])).all()
         start += c
+
+
+def test_c5_two_pow_32_keys_one_gpu(cuda):
+    """C5's whole table on one GPU: 2^32 u32 keys (V = 2^32, u64 offsets, 16
+    slices of 2^28 vertices) validated on the device with its input keys; a
+    2^26-probe count-only sliced probe equals the direct-gather probe."""
+    n = 1 << 32
+    keys = cuda.empty(n, dtype=cuda.int32, device="cuda")
+    hg.generate(keys, kind=0, seed=1)
+    t = hg.build_v2(keys)
+    assert t.num_vertices() == n and t.num_edges() == n and t.off_width == 8
+    assert hg.validate_csr(t, n, keys) is None
+    m = 1 << 26
+    probes = cuda.cat([keys[: m // 2], keys[n // 2: n // 2 + m // 2] ^ 0x3C3C3C3C])
+    res, res1 = (cuda.zeros(2, dtype=cuda.int64, device="cuda") for _ in range(2))
+    hg.probe_device(t, probes, res)
+    hg.probe_device(t, probes, res1, method=1)
+    assert res.tolist() == res1.tolist() and int(res[0]) >= m // 2
+    t.close()
