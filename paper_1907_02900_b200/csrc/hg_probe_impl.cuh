@@ -624,7 +624,11 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
               uint32_t pshift, const OffT* __restrict__ offs, const K* __restrict__ tkeys,
               const VT* __restrict__ tvals, uint32_t kcap, uint32_t pcap, uint64_t* __restrict__ status,
               void* __restrict__ pairs, uint64_t cap, uint64_t* __restrict__ totals,
-              uint32_t* ticket) {
+              uint32_t* ticket, uint64_t in_cap, const uint32_t* __restrict__ slack_flag) {
+    // probe entries of partition p: slack layout (p * in_cap) unless it
+    // overflowed, else dense (ppart[p]); pairs carry probe positions, so only
+    // the reads move
+    const bool slack_in = in_cap && !*slack_flag;
     using PE = EntryT<K, IT>;
     using PEnt = typename PE::T;
     using L = ProbeLayout<K, OffT, PEnt>;
@@ -663,14 +667,14 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
                 const uint64_t tb = offs[vb], te = offs[vb + pv];
                 const uint64_t q0 = ppart[p], q1 = ppart[p + 1];
                 s_tb = tb;
-                s_q0 = q0;
-                s_q1 = q1;
+                s_q0 = slack_in ? p * in_cap : q0;  // input start
+                s_q1 = s_q0 + (q1 - q0);
                 s_kst = te - tb <= kcap;
                 s_pst = pcap && q1 - q0 <= pcap;
                 fence_proxy_async();
                 const uintptr_t ao = reinterpret_cast<uintptr_t>(offs + vb);
                 const uintptr_t ak = reinterpret_cast<uintptr_t>(tkeys + tb);
-                const uintptr_t ae = reinterpret_cast<uintptr_t>(pin + q0);
+                const uintptr_t ae = reinterpret_cast<uintptr_t>(pin + s_q0);
                 auto span = [](uintptr_t a, size_t bytes, uint32_t& lo_off) -> uint32_t {
                     const uintptr_t lo = a & ~uintptr_t(15), hi = (a + bytes + 15) & ~uintptr_t(15);
                     lo_off = uint32_t(a - lo);
@@ -934,15 +938,19 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
     using E1 = typename EntryT<K, IT>::T;
     using E0 = typename EntryT<K, void>::T;
     const size_t ent = need_idx ? sizeof(E1) : sizeof(E0);
-    // count-only probes: slack (histogram-free) partition layout when it fits
-    // (partition_slack in hg_radix.cuh; the flag word is ticket + 2)
-    const Slack sl_caps = need_idx ? Slack{} : make_slack<OffT>(g, a.m, t.nv, nullptr);
+    const bool single = a.pairs && !want_counts && a.cap > 0;  // k_probe_pairs
+    // slack (histogram-free) partition layout when it fits (partition_slack in
+    // hg_radix.cuh; the flag word is ticket + 2): count-only probes, per-probe
+    // counts in probe order and the single-pass pairs read their partitions
+    // through it; the two-pass pairs address per-probe arrays by partitioned
+    // position and keep the dense layout
+    const bool slack_ok = !need_idx || (want_counts && !a.pairs) || single;
+    const Slack sl_caps = slack_ok ? make_slack<OffT>(g, a.m, t.nv, nullptr) : Slack{};
     const uint64_t nb1 = (g.nparts + (uint64_t(1) << g.b2) - 1) >> g.b2;
-    const size_t pscr = need_idx ? PartitionScratch<K, IT, OffT>::bytes(g, a.m)
+    const size_t pscr = need_idx ? PartitionScratch<K, IT, OffT>::bytes(g, a.m, nb1 * sl_caps.cap1)
                                  : PartitionScratch<K, void, OffT>::bytes(g, a.m, nb1 * sl_caps.cap1);
     const size_t reorg_bytes =
         (std::max<uint64_t>(a.m, g.nparts * sl_caps.cap2) * ent + 255) & ~size_t(255);
-    const bool single = a.pairs && !want_counts && a.cap > 0;  // k_probe_pairs
     const size_t cnt_bytes = (a.pairs && !single) ? ((a.m * 4 + 255) & ~size_t(255)) : 0;
     const size_t po_bytes = single ? ((g.nparts * 8 + 255) & ~size_t(255))
                                    : a.pairs ? (((a.m + 1) * 8 + 255) & ~size_t(255)) : 0;
@@ -996,10 +1004,11 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
     };
     do {
         if (need_idx) {
+            if ((e = cudaMemsetAsync(ticket, 0, 16, s)) != cudaSuccess) break;
             e = partition<K, IT, OffT, POW2>(probes, static_cast<const IT*>(nullptr), a.m, t.seed,
                                              t.hash_kind, nv, g, ppart, pscratch,
                                              static_cast<E1*>(reorg), s, kProbePassNames,
-                                             static_cast<const E1*>(a.records));
+                                             static_cast<const E1*>(a.records), 0, &sl);
         } else {
             if ((e = cudaMemsetAsync(ticket, 0, 16, s)) != cudaSuccess) break;
             e = partition<K, void, OffT, POW2>(probes, static_cast<const void*>(nullptr), a.m,
@@ -1023,8 +1032,8 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
                       kern<<<gk, kPartProbeBlock, smem, s>>>(
                           static_cast<const E1*>(reorg), ppart, g.nparts, t.nv, t.seed,
                           t.hash_kind, nv, g.pshift, offs, tkeys, tvals, kcap, pcap, pc, po, pr,
-                          cap, a.totals, ticket, (pc == a.counts && pc) ? hq : HeavyQueue{}, 0,
-                          ticket + 2));
+                          cap, a.totals, ticket, (pc == a.counts && pc) ? hq : HeavyQueue{},
+                          (pc == a.counts && pc) ? in_cap : 0, sl.flag));
             return cudaGetLastError();
         };
         // the pairs kernel reads its probe entries straight from global memory
@@ -1047,7 +1056,7 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
                       kern<<<gk, kPartProbeBlock, smem, s>>>(
                           static_cast<const E1*>(reorg), ppart, g.nparts, t.nv, t.seed,
                           t.hash_kind, nv, g.pshift, offs, tkeys, tvals, kcap_pairs, 0, status,
-                          a.pairs, a.cap, a.totals, ticket));
+                          a.pairs, a.cap, a.totals, ticket, in_cap, sl.flag));
             return cudaGetLastError();
         };
         if (!need_idx) {
