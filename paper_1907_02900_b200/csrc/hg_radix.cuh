@@ -258,6 +258,8 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
     //   in bounds, over the region's end instead.
     // in_end != nullptr (PASS2): input bucket b is [b * in_cap, in_end[b]).
     if (guard && !*guard) return;
+    // slack pass 2 after an overflowing pass 1: the exact path redoes it
+    if (out_cap && in_end && *reinterpret_cast<volatile const uint32_t*>(overflow)) return;
     using ET = EntryT<K, VT>;
     using E = typename ET::T;
     using L = SplitLayout<K, VT, RAW>;
@@ -279,17 +281,18 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
     __shared__ OffT s_gbo[kMaxDigits];
     __shared__ uint32_t s_wsum[kSplitBlock / 32];
     __shared__ uint64_t s_tp[PASS2 ? kMaxDigits + 1 : 1];  // tile_prefix cache
-    __shared__ uint64_t s_bs[PASS2 ? kMaxDigits + 1 : 1];  // bucket start cache
+    // bucket start cache (dense layout) / bucket end cache (slack layout,
+    // where bucket b starts at b * in_cap)
+    __shared__ uint64_t s_bs[PASS2 ? kMaxDigits + 1 : 1];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t ndig = dmask + 1;
 
-    // (no static bucket-end cache: p6b's shared memory must stay within two
-    // CTAs per SM; the slack layout's bucket end is read per tile instead)
     if constexpr (PASS2) {
         for (uint32_t b = tid; b <= nb1; b += kSplitBlock) {
             s_tp[b] = tile_prefix[b];
             if (in_end) {
-                s_bs[b] = uint64_t(b) * in_cap;
+                const uint64_t e = b < nb1 ? uint64_t(in_end[b]) : 0, lim = uint64_t(b + 1) * in_cap;
+                s_bs[b] = e < lim ? e : lim;
             } else {
                 const uint64_t q = (uint64_t(b) << b2) < nparts ? (uint64_t(b) << b2) : nparts;
                 s_bs[b] = part_start[q];
@@ -297,20 +300,21 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
         }
         __syncthreads();
     }
-    // (thread 0) range of a tile; false when past the last real tile
+    // (thread 0) range of a tile; false when past the last real tile. A CTA's
+    // tiles only increase, so its bucket is tracked by a forward walk (no
+    // search, no global load: the refill sits in front of a block barrier).
+    uint32_t lo = 0;
     auto tile_range = [&](uint64_t tile, uint64_t& t0, uint64_t& t1, uint64_t& cbase) -> bool {
         if constexpr (PASS2) {
             if (tile >= s_tp[nb1]) return false;
-            uint32_t lo = 0, hi = nb1;
-            while (hi - lo > 1) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (s_tp[mid] <= tile) lo = mid; else hi = mid;
-            }
-            t0 = s_bs[lo] + (tile - s_tp[lo]) * kTile;
-            uint64_t be = s_bs[lo + 1];
+            while (s_tp[lo + 1] <= tile) ++lo;
+            uint64_t be;
             if (in_end) {
-                const uint64_t e = uint64_t(in_end[lo]);
-                be = e < s_bs[lo] + in_cap ? e : s_bs[lo] + in_cap;
+                t0 = uint64_t(lo) * in_cap + (tile - s_tp[lo]) * kTile;
+                be = s_bs[lo];
+            } else {
+                t0 = s_bs[lo] + (tile - s_tp[lo]) * kTile;
+                be = s_bs[lo + 1];
             }
             t1 = be < t0 + kTile ? be : t0 + kTile;
             cbase = uint64_t(lo) << b2;
@@ -322,9 +326,12 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
         }
         return true;
     };
-    auto issue = [&](uint64_t tile, int st) {
+    auto issue = [&](uint64_t tile, int st, uint32_t abort) {
         uint64_t t0 = 0, t1 = 0, cb = 0;
-        const bool ok = tile_range(tile, t0, t1, cb);
+        // a slack layout that already overflowed (skewed keys) stops early:
+        // the exact path redoes the pass. Stages issued before stay valid and
+        // are consumed, so no bulk copy is in flight when the CTA exits.
+        const bool ok = !abort && tile_range(tile, t0, t1, cb);
         s_ok[st] = ok;
         s_t0[st] = t0;
         s_t1[st] = t1;
@@ -339,17 +346,26 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
     if (tid == 0) {
         for (int st = 0; st < kSplitStages; ++st) mbar_init(&s_bar[st], 1);
         fence_mbar_init();
-        for (int st = 0; st < kSplitStages - 1; ++st) issue(blockIdx.x + uint64_t(st) * gridDim.x, st);
+        for (int st = 0; st < kSplitStages - 1; ++st) issue(blockIdx.x + uint64_t(st) * gridDim.x, st, 0u);
     }
     __syncthreads();
     uint64_t tile = blockIdx.x;
     int st = 0;
     uint32_t phase = 0;
+    // (thread 0) overflow flag, polled every 16th tile and used one tile
+    // later, so the load's latency stays off the refill path. Only for 16-byte
+    // entries (C3's u64 keys + values, where a wasted pass costs the most):
+    // measured on the 8-byte passes of C2, even this poll costs K6a 2-4 %.
+    constexpr bool kPoll = sizeof(E) >= 16;
+    uint32_t ovf = 0, iter = 0;
     for (;; tile += gridDim.x) {
         if (!s_ok[st]) break;
         // refill the stage consumed in the previous iteration
         const int pf = st == 0 ? kSplitStages - 1 : st - 1;
-        if (tid == 0) issue(tile + uint64_t(kSplitStages - 1) * gridDim.x, pf);
+        if (tid == 0) {
+            issue(tile + uint64_t(kSplitStages - 1) * gridDim.x, pf, ovf);
+            if (kPoll && out_cap && (++iter & 15) == 0) ovf = *reinterpret_cast<volatile const uint32_t*>(overflow);
+        }
         const uint64_t t0 = s_t0[st];
         const uint32_t cnt = uint32_t(s_t1[st] - t0);
         const uint64_t cbase = s_cb[st];
@@ -566,10 +582,11 @@ struct Slack {
     uint32_t* flag = nullptr;  // device, zeroed by the caller
 };
 
-// ~8 sigma of a Poisson count above its mean: the slack capacity of a region
-// expecting `mean` entries.
-inline uint64_t slack_cap(double mean) {
-    return uint64_t(mean + 8.0 * std::sqrt(mean > 1.0 ? mean : 1.0) + 64.0);
+// Slack capacity of a region expecting `mean` entries: `factor` x the mean
+// (room for duplicated keys, e.g. multiplicity 32 widens a 4096-entry
+// partition's spread from 64 to ~360) plus 8 sigma of a Poisson count.
+inline uint64_t slack_cap(double mean, double factor) {
+    return uint64_t(factor * mean + 8.0 * std::sqrt(mean > 1.0 ? mean : 1.0) + 64.0);
 }
 
 // Slack capacities for n entries over geometry g (two passes), or none
@@ -580,8 +597,8 @@ inline Slack make_slack(const PartGeom& g, uint64_t n, uint64_t nv, uint32_t* fl
     if (g.b2 == 0 || n < (uint64_t(1) << 20)) return sl;
     const uint32_t nb1 = uint32_t((g.nparts + (uint64_t(1) << g.b2) - 1) >> g.b2);
     const double per_vertex = double(n) / double(nv);
-    sl.cap2 = slack_cap(per_vertex * double(uint64_t(1) << g.pshift));
-    sl.cap1 = slack_cap(per_vertex * double(uint64_t(1) << (g.pshift + g.b2)));
+    sl.cap2 = slack_cap(per_vertex * double(uint64_t(1) << g.pshift), 1.5);
+    sl.cap1 = slack_cap(per_vertex * double(uint64_t(1) << (g.pshift + g.b2)), 1.25);
     sl.flag = flag;
     const uint64_t lim = sizeof(OffT) == 4 ? (uint64_t(1) << 32) - 1 : ~uint64_t(0) >> 2;
     if (double(nb1) * double(sl.cap1) >= double(lim) || double(g.nparts) * double(sl.cap2) >= double(lim))
@@ -678,8 +695,9 @@ cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, 
         unsigned grid = unsigned(std::max(1, per_sm) * sms);
         grid = unsigned(std::max<uint64_t>(
             1, std::min<uint64_t>(grid, (n + kHistBlock * 16 - 1) / (kHistBlock * 16))));
-        HG_LAUNCH(names[0], s, kh<<<grid, kHistBlock, hsmem, s>>>(in, n, seed, hk, nv, g.pshift,
-                                                            uint32_t(g.nparts), hist, guard));
+        HG_LAUNCH(guard ? "fallback_hist" : names[0], s,
+                  kh<<<grid, kHistBlock, hsmem, s>>>(in, n, seed, hk, nv, g.pshift,
+                                                     uint32_t(g.nparts), hist, guard));
         return cudaGetLastError();
     };
     if constexpr (EntryT<K, VT>::kHasVal) {
@@ -690,27 +708,27 @@ cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, 
     }
     if (e != cudaSuccess) return e;
     if ((e = launch_scan<OffT, OffT>(hist, part_start, g.nparts, scan_scr, part_start + g.nparts, s,
-                                     "part_scan", guard)) != cudaSuccess)
+                                     guard ? "fallback_scan" : "part_scan", guard)) != cudaSuccess)
         return e;
     k_init_cursors<OffT><<<gi, 256, 0, s>>>(part_start, g.nparts, g.b2, nb1, cur1, cur2, guard);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (g.b2 == 0) {
         // single pass straight into partition order
-        HG_LAUNCH(names[1], s,
+        HG_LAUNCH(guard ? "fallback_split1" : names[1], s,
                   (ks1<<<g1, kSplitBlock, sm1, s>>>(
                       in1, vals, val_base, n, seed, hk, nv, g.pshift, 0, uint32_t((1u << g.b1) - 1),
                       0, cur2, part_start, 0, nullptr, tiles1, g.nparts, out, guard, 0, nullptr,
                       nullptr, 0)));
         return cudaGetLastError();
     }
-    HG_LAUNCH(names[1], s,
+    HG_LAUNCH(guard ? "fallback_split1" : names[1], s,
               (ks1<<<g1, kSplitBlock, sm1, s>>>(
                   in1, vals, val_base, n, seed, hk, nv, g.pshift, g.b2, uint32_t((1u << g.b1) - 1), 0,
                   cur1, part_start, 0, nullptr, tiles1, g.nparts, mid, guard, 0, nullptr, nullptr, 0)));
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     k_tile_prefix<OffT><<<1, kMaxDigits, 0, s>>>(part_start, g.nparts, nb1, g.b2, kSplitTile,
                                                  tile_prefix, guard, nullptr, 0);
-    HG_LAUNCH(names[2], s,
+    HG_LAUNCH(guard ? "fallback_split2" : names[2], s,
               (ks2<<<g2, kSplitBlock, sm2, s>>>(
                   mid, nullptr, 0, n, seed, hk, nv, g.pshift, 0, uint32_t((1u << g.b2) - 1), g.b2,
                   cur2, part_start, nb1, tile_prefix, tiles2, g.nparts, out, guard, 0, nullptr,

@@ -37,7 +37,31 @@ for cap, names in ROWS.items():
         continue
     rows = list(csv.reader(open(path)))
     hdr, units = rows[0], rows[1]
-    for name, r in zip(names, rows[2:]):
+    data = rows[2:]
+    if cap.endswith("_full"):
+        # classify by kernel name in launch order; guarded no-op launches (the
+        # slack layout's exact fallback, < 20 us) are skipped
+        names, keep, phase, nsplit = [], [], "k", 0
+        ti = hdr.index("gpu__time_duration.sum")
+        for r in data:
+            kn = r[hdr.index("Kernel Name")]
+            if float(r[ti]) * UNIT.get(units[ti], 1.0) < 0.02:
+                continue
+            if kn.startswith("void k_part_hist"):
+                nm = f"{phase}4_part_hist"
+            elif kn.startswith("void k_multisplit"):
+                nm = f"{phase}6{'ab'[nsplit % 2]}_multisplit"
+                nsplit += 1
+            elif kn.startswith("void k_part_build"):
+                nm, phase, nsplit = "k7_part_build", "p", 0
+            elif kn.startswith("void k_probe_part"):
+                nm = "k8p_probe_part"
+            else:
+                continue
+            names.append(nm)
+            keep.append(r)
+        data = keep
+    for name, r in zip(names, data):
         def val(m):
             i = hdr.index(m)
             return float(r[i]) * UNIT.get(units[i], 1.0)
