@@ -70,10 +70,6 @@ __device__ __forceinline__ void st_pair(void* pairs, int pair8, uint64_t slot, u
     else reinterpret_cast<uint2*>(pairs)[slot] = make_uint2(uint32_t(l), uint32_t(r));
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(

@@ -208,11 +208,15 @@ constexpr int kSplitBlock = 512;
 constexpr int kSplitStages = HG_SPLIT_STAGES;  // TMA input stages (one tile prefetched ahead)
 constexpr int kMaxDigits = 256;
 constexpr uint32_t kOwnerRun = 64;  // digit runs up to this long are filled by their owner
-// 4096-entry tiles for <= 8-byte entries, 2048 for 16-byte ones.
+// Consumer threads of a pass: pass 2 runs one producer warp (TMA refills)
+// beside 15 consumer warps, pass 1 lets thread 0 issue its (cheap) refills.
+template <bool PASS2>
+__host__ __device__ constexpr int split_cons() { return PASS2 ? kSplitBlock - 32 : kSplitBlock; }
+// 16 / 8 / 4 entries per consumer thread for 4- / 8- / 16-byte entries.
 template <typename E>
 __host__ __device__ constexpr int split_items() { return sizeof(E) >= 16 ? 4 : sizeof(E) <= 4 ? 16 : 8; }
-template <typename E>
-__host__ __device__ constexpr int split_tile() { return kSplitBlock * split_items<E>(); }
+template <typename E, bool PASS2 = false>
+__host__ __device__ constexpr int split_tile() { return split_cons<PASS2>() * split_items<E>(); }
 
 // One radix pass. RAW: input is the raw key array (+ optional vals, else the
 // input position is the value). Otherwise input is an entry array.
@@ -225,25 +229,25 @@ __host__ __device__ constexpr int split_tile() { return kSplitBlock * split_item
 // Input tiles are double-buffered in shared memory by TMA 1-D bulk copies
 // (cp.async.bulk + mbarrier): tile i+1 streams in while tile i is ranked,
 // staged digit-sorted in shared memory and written out in coalesced runs.
-template <typename K, typename VT, bool RAW>
+template <typename K, typename VT, bool RAW, bool PASS2 = false>
 struct SplitLayout {
     using E = typename EntryT<K, VT>::T;
     using InT = typename std::conditional<RAW, K, E>::type;
     static constexpr int kItems = split_items<E>();
-    static constexpr int kTile = split_tile<E>();
+    static constexpr int kTile = split_tile<E, PASS2>();
     static constexpr size_t kInBytes = (size_t(kTile) * sizeof(InT) + 32 + 15) & ~size_t(15);
     static constexpr size_t kBytes = kSplitStages * kInBytes + size_t(kTile) * sizeof(E) + kTile + 16;
 };
 
 // CTAs per SM the layout allows (<= 227 KB of shared memory per SM): 3 when
 // the tile buffers are small, else 2; the register cap follows from it.
-template <typename K, typename VT, bool RAW>
+template <typename K, typename VT, bool RAW, bool PASS2 = false>
 constexpr int split_min_blocks() {
-    return SplitLayout<K, VT, RAW>::kBytes * 3 <= size_t(220) * 1024 ? 3 : 2;
+    return SplitLayout<K, VT, RAW, PASS2>::kBytes * 3 <= size_t(220) * 1024 ? 3 : 2;
 }
 
 template <typename K, typename VT, typename OffT, bool RAW, bool PASS2, int POW2>
-__global__ void __launch_bounds__(kSplitBlock, (split_min_blocks<K, VT, RAW>()))
+__global__ void __launch_bounds__(kSplitBlock, (split_min_blocks<K, VT, RAW, PASS2>()))
 k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t val_base,
              uint64_t n, uint64_t seed,
              int hk, Divisor nv, uint32_t pshift, uint32_t dshift, uint32_t dmask, uint32_t b2,
@@ -262,14 +266,23 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
     if (out_cap && in_end && *reinterpret_cast<volatile const uint32_t*>(overflow)) return;
     using ET = EntryT<K, VT>;
     using E = typename ET::T;
-    using L = SplitLayout<K, VT, RAW>;
+    using L = SplitLayout<K, VT, RAW, PASS2>;
     using InT = typename L::InT;
     constexpr int kItems = L::kItems;
     constexpr int kTile = L::kTile;
+    // pass 2 is warp-specialised: a producer warp streams the input tiles
+    // (full / empty mbarriers per stage), so its refill -- forward bucket
+    // walk, bulk-copy issue, overflow poll -- never sits in front of the
+    // consumers' barrier (with thread 0 issuing it did: ~15 % of K6b's stall
+    // samples). Pass 1's refill is a multiply, so thread 0 keeps issuing it
+    // and all 16 warps rank.
+    constexpr bool kProd = PASS2;
+    constexpr uint32_t kCons = split_cons<PASS2>();
     extern __shared__ __align__(128) unsigned char smem[];
     E* const s_ent = reinterpret_cast<E*>(smem + kSplitStages * L::kInBytes);
     uint8_t* const s_dig = reinterpret_cast<uint8_t*>(s_ent + kTile);
-    __shared__ uint64_t s_bar[kSplitStages];
+    __shared__ uint64_t s_bar[kSplitStages];    // stage full (TMA landed)
+    __shared__ uint64_t s_empty[kSplitStages];  // stage consumed (producer mode)
     __shared__ uint64_t s_t0[kSplitStages], s_t1[kSplitStages], s_cb[kSplitStages];
     __shared__ uint32_t s_ofs[kSplitStages], s_ok[kSplitStages];
     __shared__ uint32_t s_cnt[kMaxDigits];
@@ -337,18 +350,51 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
         s_t1[st] = t1;
         s_cb[st] = cb;
         if (ok) {
+            // s_ofs is written before the arrive below releases the stage
+            const uintptr_t a = reinterpret_cast<uintptr_t>(static_cast<const InT*>(in) + t0);
+            const uintptr_t alo = a & ~uintptr_t(15);
+            const uint32_t len = uint32_t(((a + (t1 - t0) * sizeof(InT) + 15) & ~uintptr_t(15)) - alo);
+            s_ofs[st] = uint32_t(a - alo);
             fence_proxy_async();
-            s_ofs[st] = tma_load_span(smem + st * L::kInBytes, static_cast<const InT*>(in) + t0,
-                                      uint32_t((t1 - t0) * sizeof(InT)), &s_bar[st]);
+            mbar_arrive_expect_tx(&s_bar[st], len);
+            tma_load_1d(smem + st * L::kInBytes, reinterpret_cast<const void*>(alo), len, &s_bar[st]);
         }
     };
 
     if (tid == 0) {
-        for (int st = 0; st < kSplitStages; ++st) mbar_init(&s_bar[st], 1);
+        for (int st = 0; st < kSplitStages; ++st) {
+            mbar_init(&s_bar[st], 1);
+            mbar_init(&s_empty[st], 1);
+        }
         fence_mbar_init();
-        for (int st = 0; st < kSplitStages - 1; ++st) issue(blockIdx.x + uint64_t(st) * gridDim.x, st, 0u);
+        if constexpr (!kProd)
+            for (int st = 0; st < kSplitStages - 1; ++st) issue(blockIdx.x + uint64_t(st) * gridDim.x, st, 0u);
     }
     __syncthreads();
+    if constexpr (kProd) {
+        if (tid >= kCons) {
+            if (tid == kCons) {
+                uint32_t abort = 0;
+                for (uint64_t i = 0;; ++i) {
+                    const int sp = int(i % kSplitStages);
+                    if (i >= uint64_t(kSplitStages))
+                        mbar_wait(&s_empty[sp], uint32_t((i / kSplitStages - 1) & 1));
+                    issue(blockIdx.x + i * gridDim.x, sp, abort);
+                    if (!s_ok[sp]) {
+                        mbar_arrive(&s_bar[sp]);  // releases s_ok = 0: the consumers stop
+                        break;
+                    }
+                    if (out_cap) abort = *reinterpret_cast<volatile const uint32_t*>(overflow);
+                }
+            }
+            return;
+        }
+    }
+    // block barrier of the consumers (the producer warp never joins it)
+    auto bsync = [] {
+        if constexpr (kProd) asm volatile("bar.sync 1, %0;" ::"n"(kCons) : "memory");
+        else __syncthreads();
+    };
     uint64_t tile = blockIdx.x;
     int st = 0;
     uint32_t phase = 0;
@@ -359,27 +405,34 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
     constexpr bool kPoll = sizeof(E) >= 16;
     uint32_t ovf = 0, iter = 0;
     for (;; tile += gridDim.x) {
-        if (!s_ok[st]) break;
-        // refill the stage consumed in the previous iteration
-        const int pf = st == 0 ? kSplitStages - 1 : st - 1;
-        if (tid == 0) {
-            issue(tile + uint64_t(kSplitStages - 1) * gridDim.x, pf, ovf);
-            if (kPoll && out_cap && (++iter & 15) == 0) ovf = *reinterpret_cast<volatile const uint32_t*>(overflow);
+        if constexpr (kProd) {
+            for (uint32_t d = tid; d < ndig; d += kCons) s_cnt[d] = 0;
+            if (tid == 0) s_nlong = 0;
+            mbar_wait(&s_bar[st], phase);
+            if (!s_ok[st]) break;
+        } else {
+            if (!s_ok[st]) break;
+            // refill the stage consumed in the previous iteration
+            const int pf = st == 0 ? kSplitStages - 1 : st - 1;
+            if (tid == 0) {
+                issue(tile + uint64_t(kSplitStages - 1) * gridDim.x, pf, ovf);
+                if (kPoll && out_cap && (++iter & 15) == 0) ovf = *reinterpret_cast<volatile const uint32_t*>(overflow);
+            }
+            for (uint32_t d = tid; d < ndig; d += kCons) s_cnt[d] = 0;
+            if (tid == 0) s_nlong = 0;
+            mbar_wait(&s_bar[st], phase);
         }
         const uint64_t t0 = s_t0[st];
         const uint32_t cnt = uint32_t(s_t1[st] - t0);
         const uint64_t cbase = s_cb[st];
-        for (uint32_t d = tid; d < ndig; d += kSplitBlock) s_cnt[d] = 0;
-        if (tid == 0) s_nlong = 0;
-        mbar_wait(&s_bar[st], phase);
         const InT* src = reinterpret_cast<const InT*>(smem + st * L::kInBytes + s_ofs[st]);
-        __syncthreads();
+        bsync();
 
         E ent[kItems];
         uint32_t dr[kItems];  // digit << 16 | rank
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
-            const uint32_t j = tid + k * kSplitBlock;
+            const uint32_t j = tid + k * kCons;
             if (j < cnt) {
                 K key;
                 if constexpr (RAW) {
@@ -398,7 +451,7 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
                 dr[k] = (d << 16) | atomicAdd(s_cnt + d, 1u);
             }
         }
-        __syncthreads();
+        bsync();
         // exclusive scan of the <= 256 digit counts + run reservation
         const uint32_t c = tid < ndig ? s_cnt[tid] : 0;
         uint32_t inc = c;
@@ -408,7 +461,7 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
             if (int(lane) >= d) inc += y;
         }
         if (lane == 31) s_wsum[warp] = inc;
-        __syncthreads();
+        bsync();
         OffT gb = 0;
         uint32_t off = 0;
         if (tid < ndig) {
@@ -444,10 +497,10 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
                 s_long[atomicAdd(&s_nlong, 1u)] = tid;
             }
         }
-        __syncthreads();
+        bsync();
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
-            const uint32_t j = tid + k * kSplitBlock;
+            const uint32_t j = tid + k * kCons;
             if (j < cnt) s_ent[s_off[dr[k] >> 16] + (dr[k] & 0xFFFFu)] = ent[k];
         }
         for (uint32_t li = 0; li < s_nlong; ++li) {
@@ -455,7 +508,7 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
             const uint32_t o = s_off[d], e = o + s_cnt[d];
             const uint32_t w0 = (o + 3) >> 2, w1 = e >> 2;  // whole words inside the run
             const uint32_t w4 = d * 0x01010101u;
-            for (uint32_t w = w0 + tid; w < w1; w += kSplitBlock)
+            for (uint32_t w = w0 + tid; w < w1; w += kCons)
                 reinterpret_cast<uint32_t*>(s_dig)[w] = w4;
             if (tid < 4) {
                 if (o + tid < 4 * w0) s_dig[o + tid] = uint8_t(d);
@@ -463,13 +516,16 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
             }
         }
         if (c) s_gbo[tid] = gb - OffT(off);
-        __syncthreads();
+        bsync();
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
-            const uint32_t j = tid + k * kSplitBlock;
+            const uint32_t j = tid + k * kCons;
             if (j < cnt) out[uint64_t(OffT(s_gbo[s_dig[j]] + OffT(j)))] = s_ent[j];
         }
-        __syncthreads();
+        bsync();
+        if constexpr (kProd) {
+            if (tid == 0) mbar_arrive(&s_empty[st]);  // stage st free for the producer
+        }
         if (++st == kSplitStages) {
             st = 0;
             phase ^= 1;
@@ -632,15 +688,16 @@ cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, 
     cudaError_t e = cudaSuccess;
     const int sms = num_sms();
     const uint32_t nb1 = uint32_t((g.nparts + (uint64_t(1) << g.b2) - 1) >> g.b2);
-    constexpr int kSplitTile = split_tile<E>();
+    constexpr int kSplitTile = split_tile<E>();         // pass 1
+    constexpr int kSplitTile2 = split_tile<E, true>();  // pass 2 (15 consumer warps)
     const uint64_t tiles1 = (n + kSplitTile - 1) / kSplitTile;
-    const uint64_t tiles2 = tiles1 + nb1;  // upper bound; exact count = tile_prefix[nb1]
+    const uint64_t tiles2 = (n + kSplitTile2 - 1) / kSplitTile2 + nb1;  // upper bound; exact = tile_prefix[nb1]
     // pass 1 reads the raw keys (+ values), or routed records (entries already)
     auto ks1 = rec ? k_multisplit<K, VT, OffT, false, false, POW2>
                    : k_multisplit<K, VT, OffT, true, false, POW2>;
     auto ks2 = k_multisplit<K, VT, OffT, false, true, POW2>;
     const size_t sm1 = rec ? SplitLayout<K, VT, false>::kBytes : SplitLayout<K, VT, true>::kBytes;
-    constexpr size_t sm2 = SplitLayout<K, VT, false>::kBytes;
+    constexpr size_t sm2 = SplitLayout<K, VT, false, true>::kBytes;
     const void* in1 = rec ? static_cast<const void*>(rec) : static_cast<const void*>(keys);
     if ((e = cudaFuncSetAttribute(ks1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm1))) !=
             cudaSuccess ||
@@ -653,7 +710,7 @@ cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, 
     const unsigned g1 = unsigned(std::max<uint64_t>(
         1, std::min<uint64_t>(tiles1, uint64_t(sms) * std::max(1, occ1))));
     const unsigned g2 = unsigned(std::max<uint64_t>(
-        1, std::min<uint64_t>(tiles1 + 1, uint64_t(sms) * std::max(1, occ2))));
+        1, std::min<uint64_t>(tiles2, uint64_t(sms) * std::max(1, occ2))));
     const unsigned gi = unsigned(std::min<uint64_t>((g.nparts + 255) / 256, 1024));
 
     if (opt) {
@@ -667,7 +724,7 @@ cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, 
                       uint32_t((1u << g.b1) - 1), 0, cur1, part_start, 0, nullptr, tiles1,
                       g.nparts, mid, nullptr, slack->cap1, slack->flag, nullptr, 0)));
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        k_tile_prefix<OffT><<<1, kMaxDigits, 0, s>>>(part_start, g.nparts, nb1, g.b2, kSplitTile,
+        k_tile_prefix<OffT><<<1, kMaxDigits, 0, s>>>(part_start, g.nparts, nb1, g.b2, kSplitTile2,
                                                      tile_prefix, nullptr, cur1, slack->cap1);
         HG_LAUNCH(names[2], s,
                   (ks2<<<g2, kSplitBlock, sm2, s>>>(
@@ -726,7 +783,7 @@ cudaError_t partition(const K* keys, const VT* vals, uint64_t n, uint64_t seed, 
                   in1, vals, val_base, n, seed, hk, nv, g.pshift, g.b2, uint32_t((1u << g.b1) - 1), 0,
                   cur1, part_start, 0, nullptr, tiles1, g.nparts, mid, guard, 0, nullptr, nullptr, 0)));
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    k_tile_prefix<OffT><<<1, kMaxDigits, 0, s>>>(part_start, g.nparts, nb1, g.b2, kSplitTile,
+    k_tile_prefix<OffT><<<1, kMaxDigits, 0, s>>>(part_start, g.nparts, nb1, g.b2, kSplitTile2,
                                                  tile_prefix, guard, nullptr, 0);
     HG_LAUNCH(guard ? "fallback_split2" : names[2], s,
               (ks2<<<g2, kSplitBlock, sm2, s>>>(
