@@ -136,13 +136,25 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
         } else {
             for (uint32_t j = tid; j < pv; j += kBuildBlock) cnt[j] = 0;
         }
-        // per-item loops: kBase items unrolled, the rest only for large partitions
+        // per-item loops: kBase items unrolled, the rest only for large
+        // partitions. f(k, check): items below kFull of a partition holding
+        // at least kFull * kBuildBlock entries (nearly all of them: 3584 of a
+        // 4096 mean) run without the bounds check, so without a divergent
+        // region per item (BSSY / BSYNC / BRA were 15 % of K7's instructions)
+        constexpr int kFull = L::kBase - 2;
         auto for_items = [&](auto&& f) {
+            if (cntp >= uint32_t(kFull) * kBuildBlock) {
 #pragma unroll
-            for (int k = 0; k < L::kBase; ++k) f(k);
+                for (int k = 0; k < kFull; ++k) f(k, std::false_type{});
+#pragma unroll
+                for (int k = kFull; k < L::kBase; ++k) f(k, std::true_type{});
+            } else {
+#pragma unroll
+                for (int k = 0; k < L::kBase; ++k) f(k, std::true_type{});
+            }
             if (cntp > uint32_t(L::kBase) * kBuildBlock) {
 #pragma unroll
-                for (int k = L::kBase; k < kItems; ++k) f(k);
+                for (int k = L::kBase; k < kItems; ++k) f(k, std::true_type{});
             }
         };
         E ent[kItems];
@@ -151,15 +163,15 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
                 mbar_wait(&s_bar, phase);
                 phase ^= 1;
                 const E* src = reinterpret_cast<const E*>(inb + s_ofs);
-                for_items([&](int k) {
+                for_items([&](int k, auto chk) {
                     const uint32_t i = tid + k * kBuildBlock;
-                    if (i < cntp) ent[k] = src[i];
+                    if (!decltype(chk)::value || i < cntp) ent[k] = src[i];
                 });
             } else {
                 const E* src = reorg + in_of(p, s);
-                for_items([&](int k) {
+                for_items([&](int k, auto chk) {
                     const uint32_t i = tid + k * kBuildBlock;
-                    if (i < cntp) ent[k] = __ldcs(src + i);
+                    if (!decltype(chk)::value || i < cntp) ent[k] = __ldcs(src + i);
                 });
             }
         }
@@ -179,9 +191,9 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
         // (core.hpp:126-133); the returned count is the entry's rank
         uint32_t lr[kItems];
         if (staged) {
-            for_items([&](int k) {
+            for_items([&](int k, auto chk) {
                 const uint32_t i = tid + k * kBuildBlock;
-                if (i < cntp) {
+                if (!decltype(chk)::value || i < cntp) {
                     const uint32_t lv = uint32_t(hv<POW2>(PE::key(ent[k]), seed, hk, nv) - vb);
                     lr[k] = (lv << 16) | atomicAdd(cnt + lv, 1u);
                 }
@@ -277,9 +289,9 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
             // arrays of a vertex-range slice start at any entry)
             K* skp = sk + ((reinterpret_cast<uintptr_t>(okeys + s) / sizeof(K)) & (KA - 1));
             VT* svp = sv + ((reinterpret_cast<uintptr_t>(ovals + s) / sizeof(VT)) & (VA - 1));
-            for_items([&](int k) {
+            for_items([&](int k, auto chk) {
                 const uint32_t i = tid + k * kBuildBlock;
-                if (i < cntp) {
+                if (!decltype(chk)::value || i < cntp) {
                     const uint32_t pos = cnt[lr[k] >> 16] + (lr[k] & 0xFFFFu);
                     skp[pos] = PE::key(ent[k]);
                     svp[pos] = PE::val(ent[k]);

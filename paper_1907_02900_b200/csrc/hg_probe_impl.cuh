@@ -413,11 +413,13 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
                 // offsets' width (u32 at C2), fewer 64-bit address updates
                 using I = OffT;
                 const I qi = I(qn), tbi = I(tb);
-                for (I base = I(warp) * 32; base < qi; base += I(nwarps) * 32) {
+                // whole-warp rounds run without the bounds check (no divergent
+                // region per probe); the last, partial round checks
+                auto round = [&](I base, auto chk) {
                     const I i = base + I(lane);
                     K key = 0;
                     I b = 0, e = 0;
-                    if (i < qi) {
+                    if (!decltype(chk)::value || i < qi) {
                         key = PE::key(ep[i]);
                         const uint32_t lv = uint32_t(hv<POW2>(key, seed, hk, nv) - vb);
                         b = I(soff[lv]) - tbi;
@@ -441,7 +443,10 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
                         if (int(lane) == src) c = cc;
                     }
                     matches += c;
-                }
+                };
+                I base = I(warp) * 32;
+                for (; base + 32 <= qi; base += I(nwarps) * 32) round(base, std::false_type{});
+                if (base < qi) round(base, std::true_type{});
             } else {
                 for (uint64_t base = uint64_t(warp) * 32; base < qn; base += uint64_t(nwarps) * 32) {
                     const uint64_t i = base + lane;

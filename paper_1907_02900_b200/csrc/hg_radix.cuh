@@ -430,10 +430,16 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
 
         E ent[kItems];
         uint32_t dr[kItems];  // digit << 16 | rank
+        // full tiles (all but each bucket's last) run the per-entry loops
+        // without bounds checks: no divergent region per item (BSSY / BSYNC /
+        // BRA were 15 % of K6b's instructions)
+        const bool full = cnt == uint32_t(kTile);
+        auto rank_items = [&](auto fullc) {
+        constexpr bool F = decltype(fullc)::value;
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
             const uint32_t j = tid + k * kCons;
-            if (j < cnt) {
+            if (F || j < cnt) {
                 K key;
                 if constexpr (RAW) {
                     key = src[j];
@@ -451,6 +457,9 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
                 dr[k] = (d << 16) | atomicAdd(s_cnt + d, 1u);
             }
         }
+        };
+        if (full) rank_items(std::true_type{});
+        else rank_items(std::false_type{});
         bsync();
         // exclusive scan of the <= 256 digit counts + run reservation
         const uint32_t c = tid < ndig ? s_cnt[tid] : 0;
@@ -498,10 +507,15 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
             }
         }
         bsync();
+        if (full) {
 #pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-            const uint32_t j = tid + k * kCons;
-            if (j < cnt) s_ent[s_off[dr[k] >> 16] + (dr[k] & 0xFFFFu)] = ent[k];
+            for (int k = 0; k < kItems; ++k) s_ent[s_off[dr[k] >> 16] + (dr[k] & 0xFFFFu)] = ent[k];
+        } else {
+#pragma unroll
+            for (int k = 0; k < kItems; ++k) {
+                const uint32_t j = tid + k * kCons;
+                if (j < cnt) s_ent[s_off[dr[k] >> 16] + (dr[k] & 0xFFFFu)] = ent[k];
+            }
         }
         for (uint32_t li = 0; li < s_nlong; ++li) {
             const uint32_t d = s_long[li];
@@ -517,10 +531,18 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
         }
         if (c) s_gbo[tid] = gb - OffT(off);
         bsync();
+        if (full) {
 #pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-            const uint32_t j = tid + k * kCons;
-            if (j < cnt) out[uint64_t(OffT(s_gbo[s_dig[j]] + OffT(j)))] = s_ent[j];
+            for (int k = 0; k < kItems; ++k) {
+                const uint32_t j = tid + k * kCons;
+                out[uint64_t(OffT(s_gbo[s_dig[j]] + OffT(j)))] = s_ent[j];
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kItems; ++k) {
+                const uint32_t j = tid + k * kCons;
+                if (j < cnt) out[uint64_t(OffT(s_gbo[s_dig[j]] + OffT(j)))] = s_ent[j];
+            }
         }
         bsync();
         if constexpr (kProd) {
