@@ -15,3 +15,6 @@ ncu -i gpurun_out/${TAG}_full.ncu-rep --page raw --csv > gpurun_out/${TAG}_full_
 python scripts/ncu_lines.py gpurun_out/${TAG}_full.ncu-rep . 30 > gpurun_out/${TAG}_lines.txt 2>&1
 python scripts/ncu_summary.py gpurun_out/${TAG}_full.ncu-rep . 10 > gpurun_out/${TAG}_summary.txt 2>&1
 du -sh gpurun_out
+# the report itself (12 kernels with source) exceeds gpurun's 64 MiB merge cap: compress it
+xz -T0 -6 gpurun_out/${TAG}_full.ncu-rep 2>/dev/null
+du -sh gpurun_out
