@@ -123,7 +123,29 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
             n_e = part_start[p0 + step + 1];
         }
     }
+    // vertex counters: zeroed here for the first partition, then during the
+    // bulk stores of the previous one (no barrier at a partition's start)
+    auto zero_cnt = [&] {
+        if ((P & 3) == 0) {
+            for (uint32_t j = 4 * tid; j < P; j += 4 * kBuildBlock) sts128(cnt + j, make_uint4(0, 0, 0, 0));
+        } else {
+            for (uint32_t j = tid; j < P; j += kBuildBlock) cnt[j] = 0;
+        }
+    };
+    zero_cnt();
     __syncthreads();
+    // (thread 0, once every thread has read this partition's bounds and
+    // staged input) next partition's entries stream in while this one is built
+    auto advance = [&](uint64_t p) {
+        const uint64_t pn = p + step;
+        if (pn < nparts) issue(pn, n_s, n_e);
+        s_s = n_s;
+        s_e = n_e;
+        if (pn + step < nparts) {
+            n_s = part_start[pn + step];
+            n_e = part_start[pn + step + 1];
+        }
+    };
     uint32_t phase = 0;
     for (uint64_t p = blockIdx.x; p < nparts; p += step) {
         const uint64_t s = s_s, e = s_e;
@@ -131,11 +153,6 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
         const bool staged = cntp <= cap;
         const uint64_t vb = p << pshift;
         const uint32_t pv = uint32_t(nv_total - vb < P ? nv_total - vb : uint64_t(P));
-        if ((pv & 3) == 0) {
-            for (uint32_t j = 4 * tid; j < pv; j += 4 * kBuildBlock) sts128(cnt + j, make_uint4(0, 0, 0, 0));
-        } else {
-            for (uint32_t j = tid; j < pv; j += kBuildBlock) cnt[j] = 0;
-        }
         // per-item loops: kBase items unrolled, the rest only for large
         // partitions. f(k, check): items below kFull of a partition holding
         // at least kFull * kBuildBlock entries (nearly all of them: 3584 of a
@@ -175,18 +192,6 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
                 });
             }
         }
-        __syncthreads();  // cnt zeroed, input buffer consumed
-        if (tid == 0) {
-            // next partition's entries stream in while this one is built
-            const uint64_t pn = p + step;
-            if (pn < nparts) issue(pn, n_s, n_e);
-            s_s = n_s;
-            s_e = n_e;
-            if (pn + step < nparts) {
-                n_s = part_start[pn + step];
-                n_e = part_start[pn + step + 1];
-            }
-        }
         // count: the second hash evaluation of V2's create_table pass
         // (core.hpp:126-133); the returned count is the entry's rank
         uint32_t lr[kItems];
@@ -204,10 +209,13 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
             for (uint32_t j = tid; j < pv; j += kBuildBlock) offs[vb + j + 1] = OffT(0);
             if (p == 0 && tid == 0) offs[0] = OffT(obase);
             if (tid == 0) big_list[atomicAdd(big_n, 1u)] = uint32_t(p);
+            __syncthreads();  // bounds read by every thread
+            if (tid == 0) advance(p);
             __syncthreads();
             continue;
         }
-        __syncthreads();
+        __syncthreads();  // counts final; staged input and bounds consumed
+        if (tid == 0) advance(p);
         // exclusive scan of cnt[0..pv): thread owns `per` consecutive counters
         // (vectorised 16-byte shared loads/stores when per is a multiple of 4)
         const uint64_t so = s + obase;  // offsets are written with the table's entry base
@@ -234,18 +242,10 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
         }
         if (lane == 31) s_warp[warp] = inc;
         __syncthreads();
-        if (warp == 0) {
-            const uint32_t w = lane < kBuildBlock / 32 ? s_warp[lane] : 0;
-            uint32_t wi = w;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, wi, d);
-                if (int(lane) >= d) wi += y;
-            }
-            if (lane < kBuildBlock / 32) s_warp[lane] = wi - w;
-        }
-        __syncthreads();
-        uint32_t acc = s_warp[warp] + inc - run;
+        // each warp sums the totals of the warps before it (one load per
+        // lane + a warp reduction; no second barrier)
+        const uint32_t wbase = warp_sum(lane < warp ? s_warp[lane] : 0u);
+        uint32_t acc = wbase + inc - run;
         if (vec) {
             for (uint32_t q = 0; q < per; q += 4) {
                 const uint4 c4 = lds128(cnt + j0 + q);
@@ -302,6 +302,7 @@ k_part_build(const typename EntryT<K, VT>::T* __restrict__ reorg,
             const bool a = bulk_store_span(okeys + s, skp, cntp, tid, kBuildBlock);
             const bool b = bulk_store_span(ovals + s, svp, cntp, tid, kBuildBlock);
             if (a || b) bulk_commit();
+            zero_cnt();  // counters of the next partition (cnt is no longer read)
         }
         __syncthreads();
     }

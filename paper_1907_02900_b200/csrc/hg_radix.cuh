@@ -292,7 +292,6 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
     // reserved global base - tile offset of each digit, in the offsets' width
     // (modular: base - off + j is the exact output index for j >= off)
     __shared__ OffT s_gbo[kMaxDigits];
-    __shared__ uint32_t s_wsum[kSplitBlock / 32];
     __shared__ uint64_t s_tp[PASS2 ? kMaxDigits + 1 : 1];  // tile_prefix cache
     // bucket start cache (dense layout) / bucket end cache (slack layout,
     // where bucket b starts at b * in_cap)
@@ -404,10 +403,14 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
     // measured on the 8-byte passes of C2, even this poll costs K6a 2-4 %.
     constexpr bool kPoll = sizeof(E) >= 16;
     uint32_t ovf = 0, iter = 0;
+    // digit counters are zeroed here for the first tile and during the
+    // write-out of the previous tile for the others, so a tile starts without
+    // a barrier (each thread waits on the stage's mbarrier itself)
+    for (uint32_t d = tid; d < ndig; d += kCons) s_cnt[d] = 0;
+    if (tid == 0) s_nlong = 0;
+    bsync();
     for (;; tile += gridDim.x) {
         if constexpr (kProd) {
-            for (uint32_t d = tid; d < ndig; d += kCons) s_cnt[d] = 0;
-            if (tid == 0) s_nlong = 0;
             mbar_wait(&s_bar[st], phase);
             if (!s_ok[st]) break;
         } else {
@@ -418,15 +421,12 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
                 issue(tile + uint64_t(kSplitStages - 1) * gridDim.x, pf, ovf);
                 if (kPoll && out_cap && (++iter & 15) == 0) ovf = *reinterpret_cast<volatile const uint32_t*>(overflow);
             }
-            for (uint32_t d = tid; d < ndig; d += kCons) s_cnt[d] = 0;
-            if (tid == 0) s_nlong = 0;
             mbar_wait(&s_bar[st], phase);
         }
         const uint64_t t0 = s_t0[st];
         const uint32_t cnt = uint32_t(s_t1[st] - t0);
         const uint64_t cbase = s_cb[st];
         const InT* src = reinterpret_cast<const InT*>(smem + st * L::kInBytes + s_ofs[st]);
-        bsync();
 
         E ent[kItems];
         uint32_t dr[kItems];  // digit << 16 | rank
@@ -469,13 +469,16 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
             const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
             if (int(lane) >= d) inc += y;
         }
-        if (lane == 31) s_wsum[warp] = inc;
-        bsync();
+        // counts of the digits below this warp's 32, summed by the warp itself
+        // (no cross-warp partials, no barrier)
+        uint32_t base = 0;
+        if (warp * 32 < ndig) {
+            for (uint32_t w = 0; w < warp; ++w) base += s_cnt[32 * w + lane];
+            base = warp_sum(base);
+        }
         OffT gb = 0;
         uint32_t off = 0;
         if (tid < ndig) {
-            uint32_t base = 0;
-            for (uint32_t w = 0; w < warp; ++w) base += s_wsum[w];
             off = base + inc - c;
             s_off[tid] = off;
             // the run reservation is consumed only after the scatter below, so
@@ -531,6 +534,9 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
         }
         if (c) s_gbo[tid] = gb - OffT(off);
         bsync();
+        // counters of the next tile (s_cnt is not read by the write-out)
+        for (uint32_t d = tid; d < ndig; d += kCons) s_cnt[d] = 0;
+        if (tid == 0) s_nlong = 0;
         if (full) {
 #pragma unroll
             for (int k = 0; k < kItems; ++k) {
