@@ -400,13 +400,27 @@ k7b_prefix(const OffT* __restrict__ part_start, const uint32_t* __restrict__ lis
 
 // Block-aggregated variant for partitions of <= 2^14 vertices: a CTA takes a
 // 4096-entry chunk of one queued partition, counts it per vertex in shared
-// memory (warp-aggregated shared atomics), and touches the global counters /
-// cursors once per (chunk, vertex) instead of once per entry or warp -- a
-// hot key costs one global atomic per chunk. PLACE: the chunk reserves each
-// vertex's run with one global atomic, then hands out slots from shared
-// memory.
+// memory, and touches the global counters / cursors once per (chunk, vertex)
+// instead of once per entry or warp -- a hot key costs one global atomic per
+// chunk. PLACE: the chunk reserves each vertex's run with one global atomic,
+// then hands out slots from shared memory.
+// A thread loads its kBigPer entries of the chunk up front (all loads in
+// flight at once; they are issued before the counters are zeroed) and keeps
+// them, their vertices and their peer masks in registers, so PLACE reads and
+// hashes each entry once. Peer groups: a warp whose lanes all hold one vertex
+// (the common case inside a partition queued for a heavy key) skips
+// match.any.
+constexpr int kBigBlock = 512;
+constexpr int kBigPer = int(kBigChunk) / kBigBlock;
+
+__device__ __forceinline__ uint32_t big_peers(uint32_t active, uint32_t v) {
+    const uint32_t v0 = __shfl_sync(active, v, __ffs(active) - 1);
+    if (__all_sync(active, v == v0)) return active;
+    return __match_any_sync(active, v);
+}
+
 template <typename K, typename VT, typename OffT, int POW2, bool PLACE>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(kBigBlock, 2)
 k7b_chunk(const typename EntryT<K, VT>::T* __restrict__ reorg, const OffT* __restrict__ part_start,
           const uint32_t* __restrict__ list, const uint32_t* __restrict__ big_n,
           const uint64_t* __restrict__ cpref, uint64_t nv_total, uint64_t seed, Divisor nv,
@@ -419,7 +433,7 @@ k7b_chunk(const typename EntryT<K, VT>::T* __restrict__ reorg, const OffT* __res
     const uint32_t nb = *big_n;
     if (nb == 0) return;
     const uint64_t nchunks = cpref[nb];
-    const uint32_t tid = threadIdx.x;
+    const uint32_t tid = threadIdx.x, lane = tid & 31;
     const uint64_t P = uint64_t(1) << pshift;
     for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
         const uint32_t li = big_owner(cpref, nb, c);
@@ -428,22 +442,31 @@ k7b_chunk(const typename EntryT<K, VT>::T* __restrict__ reorg, const OffT* __res
         // input view at dense indices (pointer arithmetic in 64-bit indices)
         const typename PE::T* rin = reorg + (slack_in ? p * in_cap : s);
         const uint64_t c0 = s + (c - cpref[li]) * kBigChunk;
-        const uint64_t c1 = e < c0 + kBigChunk ? e : c0 + kBigChunk;
+        const uint32_t cn = uint32_t((e < c0 + kBigChunk ? e : c0 + kBigChunk) - c0);
         const uint64_t vb = p << pshift;
         const uint32_t pv = uint32_t(nv_total - vb < P ? nv_total - vb : P);
-        for (uint32_t v = tid; v < pv; v += blockDim.x) hist[v] = 0;
+        typename PE::T en[kBigPer];
+#pragma unroll
+        for (int k = 0; k < kBigPer; ++k) {
+            const uint32_t j = tid + k * kBigBlock;
+            if (j < cn) en[k] = rin[c0 - s + j];
+        }
+        for (uint32_t v = tid; v < pv; v += kBigBlock) hist[v] = 0;
         __syncthreads();
-        for (uint64_t j0 = c0; j0 < c1; j0 += blockDim.x) {
-            const uint64_t j = j0 + tid;
-            const bool act = j < c1;
+        uint32_t lv[kBigPer], peers[kBigPer];
+#pragma unroll
+        for (int k = 0; k < kBigPer; ++k) {
+            const uint32_t j = tid + k * kBigBlock;
+            const bool act = j < cn;
             const uint32_t active = __ballot_sync(0xffffffffu, act);
             if (act) {
-                const uint32_t lv = uint32_t(vhash<POW2>(PE::key(rin[j - s]), seed, nv) - vb);
-                aggregated_count<true>(hist + lv, active, lv);
+                lv[k] = uint32_t(vhash<POW2>(PE::key(en[k]), seed, nv) - vb);
+                peers[k] = big_peers(active, lv[k]);
+                if (lane == uint32_t(__ffs(peers[k]) - 1)) atom_add(hist + lv[k], OffT(__popc(peers[k])));
             }
         }
         __syncthreads();
-        for (uint32_t v = tid; v < pv; v += blockDim.x) {
+        for (uint32_t v = tid; v < pv; v += kBigBlock) {
             const OffT h = hist[v];
             if (h) {
                 const OffT base = atom_add(offs + vb + v + 1, h);
@@ -452,16 +475,18 @@ k7b_chunk(const typename EntryT<K, VT>::T* __restrict__ reorg, const OffT* __res
         }
         if constexpr (PLACE) {
             __syncthreads();
-            for (uint64_t j0 = c0; j0 < c1; j0 += blockDim.x) {
-                const uint64_t j = j0 + tid;
-                const bool act = j < c1;
-                const uint32_t active = __ballot_sync(0xffffffffu, act);
-                if (act) {
-                    const auto en = rin[j - s];
-                    const uint32_t lv = uint32_t(vhash<POW2>(PE::key(en), seed, nv) - vb);
-                    const uint64_t slot = aggregated_ticket<true>(hist + lv, active, lv);
-                    okeys[slot] = PE::key(en);
-                    ovals[slot] = PE::val(en);
+#pragma unroll
+            for (int k = 0; k < kBigPer; ++k) {
+                const uint32_t j = tid + k * kBigBlock;
+                if (j < cn) {
+                    const uint32_t pk = peers[k];
+                    const uint32_t leader = __ffs(pk) - 1;
+                    OffT base = 0;
+                    if (lane == leader) base = atom_add(hist + lv[k], OffT(__popc(pk)));
+                    base = __shfl_sync(pk, base, leader);
+                    const uint64_t slot = uint64_t(base) + __popc(pk & lanemask_lt());
+                    okeys[slot] = PE::key(en[k]);
+                    ovals[slot] = PE::val(en[k]);
                 }
             }
         }
@@ -644,9 +669,9 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
                  (e = cudaFuncSetAttribute(kc1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hsm))) !=
                      cudaSuccess))
                 break;
-            const unsigned gc = unsigned(num_sms() * 3);
+            const unsigned gc = unsigned(num_sms() * 2);
             HG_LAUNCH("k7b_big_count", s,
-                      (kc0<<<gc, 512, hsm, s>>>(reorg, part_start, big_list, big_n, big_cpref, t.nv,
+                      (kc0<<<gc, kBigBlock, hsm, s>>>(reorg, part_start, big_list, big_n, big_cpref, t.nv,
                                                t.seed, nv, g.pshift, offs, nullptr, nullptr, in_cap,
                                                sl.flag)));
             HG_LAUNCH("k7b_big_scan", s,
@@ -654,7 +679,7 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
                                                                            big_n, t.nv, g.pshift,
                                                                            t.obase, offs)));
             HG_LAUNCH("k7b_big_place", s,
-                      (kc1<<<gc, 512, hsm, s>>>(reorg, part_start, big_list, big_n, big_cpref, t.nv,
+                      (kc1<<<gc, kBigBlock, hsm, s>>>(reorg, part_start, big_list, big_n, big_cpref, t.nv,
                                                t.seed, nv, g.pshift, offs, static_cast<K*>(t.keys) - t.obase,
                                                static_cast<VT*>(t.vals) - t.obase, in_cap, sl.flag)));
             e = cudaGetLastError();
