@@ -419,14 +419,45 @@ __device__ __forceinline__ uint32_t big_peers(uint32_t active, uint32_t v) {
     return __match_any_sync(active, v);
 }
 
+// One K7b chunk task: partition p, cn entries starting at input index c0
+// (slack region or dense range of the partition; written once
+// per launch by k7b_map, so a chunk's CTA does one broadcast load instead of a
+// binary search over the queue: the search was K7b's top stall).
+struct __align__(16) BigChunk {
+    uint32_t p, cn;
+    uint64_t c0;
+};
+
+template <typename OffT>
+__global__ void __launch_bounds__(256)
+k7b_map(const OffT* __restrict__ part_start, const uint32_t* __restrict__ list,
+        const uint32_t* __restrict__ big_n, const uint64_t* __restrict__ cpref,
+        BigChunk* __restrict__ map, uint64_t in_cap, const uint32_t* __restrict__ slack_flag) {
+    const bool slack_in = in_cap && !*slack_flag;
+    const uint32_t nb = *big_n;
+    if (nb == 0) return;
+    const uint64_t nchunks = cpref[nb];
+    for (uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < nchunks;
+         c += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t li = big_owner(cpref, nb, c);
+        const uint32_t p = list[li];
+        const uint64_t s = part_start[p], e = part_start[p + 1];
+        const uint64_t c0 = s + (c - cpref[li]) * kBigChunk;
+        BigChunk b;
+        b.p = p;
+        b.cn = uint32_t((e < c0 + kBigChunk ? e : c0 + kBigChunk) - c0);
+        b.c0 = (slack_in ? uint64_t(p) * in_cap : s) + (c0 - s);  // index into the input
+        map[c] = b;
+    }
+}
+
 template <typename K, typename VT, typename OffT, int POW2, bool PLACE>
 __global__ void __launch_bounds__(kBigBlock, 2)
-k7b_chunk(const typename EntryT<K, VT>::T* __restrict__ reorg, const OffT* __restrict__ part_start,
-          const uint32_t* __restrict__ list, const uint32_t* __restrict__ big_n,
+k7b_chunk(const typename EntryT<K, VT>::T* __restrict__ reorg, const BigChunk* __restrict__ map,
+          const uint32_t* __restrict__ big_n,
           const uint64_t* __restrict__ cpref, uint64_t nv_total, uint64_t seed, Divisor nv,
           uint32_t pshift, OffT* __restrict__ offs, K* __restrict__ okeys, VT* __restrict__ ovals,
           uint64_t in_cap, const uint32_t* __restrict__ slack_flag) {
-    const bool slack_in = in_cap && !*slack_flag;
     using PE = EntryT<K, VT>;
     extern __shared__ __align__(128) unsigned char smem[];
     OffT* const hist = reinterpret_cast<OffT*>(smem);
@@ -435,23 +466,27 @@ k7b_chunk(const typename EntryT<K, VT>::T* __restrict__ reorg, const OffT* __res
     const uint64_t nchunks = cpref[nb];
     const uint32_t tid = threadIdx.x, lane = tid & 31;
     const uint64_t P = uint64_t(1) << pshift;
+    // counters start at zero; the count pass re-zeroes the ones it used
+    // while reserving, the place pass zeroes all at the start of a chunk
+    if constexpr (!PLACE) {
+        for (uint32_t v = tid; v < P; v += kBigBlock) hist[v] = 0;
+    }
     for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        const uint32_t li = big_owner(cpref, nb, c);
-        const uint64_t p = list[li];
-        const uint64_t s = part_start[p], e = part_start[p + 1];
-        // input view at dense indices (pointer arithmetic in 64-bit indices)
-        const typename PE::T* rin = reorg + (slack_in ? p * in_cap : s);
-        const uint64_t c0 = s + (c - cpref[li]) * kBigChunk;
-        const uint32_t cn = uint32_t((e < c0 + kBigChunk ? e : c0 + kBigChunk) - c0);
+        const BigChunk bc = map[c];
+        const uint64_t p = bc.p;
+        const uint32_t cn = bc.cn;
         const uint64_t vb = p << pshift;
         const uint32_t pv = uint32_t(nv_total - vb < P ? nv_total - vb : P);
+        const typename PE::T* rin = reorg + bc.c0;
         typename PE::T en[kBigPer];
 #pragma unroll
         for (int k = 0; k < kBigPer; ++k) {
             const uint32_t j = tid + k * kBigBlock;
-            if (j < cn) en[k] = rin[c0 - s + j];
+            if (j < cn) en[k] = rin[j];
         }
-        for (uint32_t v = tid; v < pv; v += kBigBlock) hist[v] = 0;
+        if constexpr (PLACE) {
+            for (uint32_t v = tid; v < pv; v += kBigBlock) hist[v] = 0;
+        }
         __syncthreads();
         uint32_t lv[kBigPer], peers[kBigPer];
 #pragma unroll
@@ -470,7 +505,7 @@ k7b_chunk(const typename EntryT<K, VT>::T* __restrict__ reorg, const OffT* __res
             const OffT h = hist[v];
             if (h) {
                 const OffT base = atom_add(offs + vb + v + 1, h);
-                if constexpr (PLACE) hist[v] = base;
+                hist[v] = PLACE ? base : OffT(0);
             }
         }
         if constexpr (PLACE) {
@@ -612,9 +647,12 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
     // K7b queue: at most nparts oversized partitions
     const size_t list_bytes = ((g.nparts + 1) * 4 + 255) & ~size_t(255);
     const size_t pref_bytes = (2 * (g.nparts + 1) * 8 + 255) & ~size_t(255);  // pref | cpref
+    // K7b chunk table: at most n / kBigChunk + nparts chunks
+    const size_t map_bytes = ((t.n / kBigChunk + g.nparts + 1) * sizeof(BigChunk) + 255) & ~size_t(255);
     char* scratch = nullptr;
     if ((e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
-                             ps_bytes + pscr + reorg_bytes + list_bytes + pref_bytes + 2048, s)) !=
+                             ps_bytes + pscr + reorg_bytes + list_bytes + pref_bytes + map_bytes + 2048,
+                             s)) !=
         cudaSuccess)
         return e;
     OffT* part_start = reinterpret_cast<OffT*>(scratch);
@@ -622,8 +660,10 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
     E* reorg = reinterpret_cast<E*>(scratch + ps_bytes + pscr);
     uint32_t* big_list = reinterpret_cast<uint32_t*>(scratch + ps_bytes + pscr + reorg_bytes);
     uint64_t* big_pref = reinterpret_cast<uint64_t*>(scratch + ps_bytes + pscr + reorg_bytes + list_bytes);
+    BigChunk* big_map = reinterpret_cast<BigChunk*>(scratch + ps_bytes + pscr + reorg_bytes + list_bytes +
+                                                    pref_bytes);
     uint32_t* ticket = reinterpret_cast<uint32_t*>(scratch + ps_bytes + pscr + reorg_bytes + list_bytes +
-                                                   pref_bytes);  // ticket, big_n, slack flag
+                                                   pref_bytes + map_bytes);  // ticket, big_n, slack flag
     Slack sl = sl_caps;
     sl.flag = ticket + 2;
     do {
@@ -670,8 +710,11 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
                      cudaSuccess))
                 break;
             const unsigned gc = unsigned(num_sms() * 2);
+            HG_LAUNCH("k7b_big_map", s,
+                      (k7b_map<OffT><<<unsigned(num_sms() * 2), 256, 0, s>>>(part_start, big_list, big_n,
+                                                                         big_cpref, big_map, in_cap, sl.flag)));
             HG_LAUNCH("k7b_big_count", s,
-                      (kc0<<<gc, kBigBlock, hsm, s>>>(reorg, part_start, big_list, big_n, big_cpref, t.nv,
+                      (kc0<<<gc, kBigBlock, hsm, s>>>(reorg, big_map, big_n, big_cpref, t.nv,
                                                t.seed, nv, g.pshift, offs, nullptr, nullptr, in_cap,
                                                sl.flag)));
             HG_LAUNCH("k7b_big_scan", s,
@@ -679,7 +722,7 @@ cudaError_t build_v2_impl(const TableDesc& t, const BuildArgs& a, cudaStream_t s
                                                                            big_n, t.nv, g.pshift,
                                                                            t.obase, offs)));
             HG_LAUNCH("k7b_big_place", s,
-                      (kc1<<<gc, kBigBlock, hsm, s>>>(reorg, part_start, big_list, big_n, big_cpref, t.nv,
+                      (kc1<<<gc, kBigBlock, hsm, s>>>(reorg, big_map, big_n, big_cpref, t.nv,
                                                t.seed, nv, g.pshift, offs, static_cast<K*>(t.keys) - t.obase,
                                                static_cast<VT*>(t.vals) - t.obase, in_cap, sl.flag)));
             e = cudaGetLastError();
