@@ -566,14 +566,14 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
 constexpr uint32_t kPairRound = 24;  // chunks per scan round (24 * 512 = 12288 probes)
 
 // Per-lane match count of probe `i` of the partition (valid < qn), with
-// warp-cooperative walks of long segments; warp-collective.
-template <typename K, typename OffT, typename PEnt, typename PE, int POW2>
+// warp-cooperative walks of long segments; warp-collective. Positions are
+// partition-relative in the offsets' width (u32 at C2/C4), probe indices in J.
+template <typename K, typename OffT, typename PEnt, typename PE, int POW2, typename J>
 __device__ __forceinline__ uint32_t pair_count(const K* __restrict__ kp, const PEnt& ent,
-                                               const OffT* soff, uint64_t i, uint64_t qn, uint64_t tb,
+                                               const OffT* soff, J i, J qn, OffT tb,
                                                uint64_t vb, uint64_t seed, int hk, const Divisor& nv,
-                                               uint64_t& compared, K& key, uint64_t& b, uint64_t& e,
+                                               uint64_t& compared, K& key, OffT& b, OffT& e,
                                                uint32_t& pos) {
-    // partition-relative positions in the offsets' width (u32 at C2)
     using I = OffT;
     const uint32_t lane = threadIdx.x & 31;
     I bi = 0, ei = 0;
@@ -581,8 +581,8 @@ __device__ __forceinline__ uint32_t pair_count(const K* __restrict__ kp, const P
     if (i < qn) {
         key = PE::key(ent);
         const uint32_t lv = uint32_t(hv<POW2>(key, seed, hk, nv) - vb);
-        bi = I(soff[lv]) - I(tb);
-        ei = I(soff[lv + 1]) - I(tb);
+        bi = I(soff[lv]) - tb;
+        ei = I(soff[lv + 1]) - tb;
     }
     const I len = ei - bi;
     compared += len;
@@ -606,6 +606,13 @@ __device__ __forceinline__ uint32_t pair_count(const K* __restrict__ kp, const P
     return c;
 }
 
+// Inclusive warp prefix of per-lane counts; one ballot when every count is
+// 0 or 1 (unique build keys: C4), else the shuffle scan.
+__device__ __forceinline__ uint32_t warp_incl_count(uint32_t c) {
+    if (__all_sync(0xffffffffu, c <= 1u)) return __popc(__ballot_sync(0xffffffffu, c != 0) & lanemask_lt()) + c;
+    return warp_inclusive_sum(c);
+}
+
 constexpr uint32_t kNeedWalk = 0xFFFFFFFFu;
 
 // Shared bytes of the single-pass pairs kernel's staged table-value slice.
@@ -616,13 +623,14 @@ __host__ __device__ constexpr size_t pair_val_bytes(uint32_t kcap) {
 
 // Pass-A summary of one probe for pass B: 0 (no match), (t << 16) | 1 (one
 // match at tile key t = b + pos, short segment, t < 2^16) or kNeedWalk.
-__device__ __forceinline__ uint32_t pair_info(uint64_t b, uint64_t e, uint32_t c, uint32_t pos) {
+template <typename I>
+__device__ __forceinline__ uint32_t pair_info(I b, I e, uint32_t c, uint32_t pos) {
     if (c == 0) return 0u;
-    if (c != 1 || e - b > kLongSeg || e > 0xFFFFu) return kNeedWalk;
+    if (c != 1 || e - b > I(kLongSeg) || e > I(0xFFFFu)) return kNeedWalk;
     return (uint32_t(b + pos) << 16) | 1u;
 }
 
-template <typename K, typename VT, typename OffT, typename IT, int POW2, typename PT>
+template <typename K, typename VT, typename OffT, typename IT, int POW2, typename PT, typename PJ>
 __global__ void __launch_bounds__(kPartProbeBlock)
 k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __restrict__ ppart,
               uint64_t nparts, uint64_t nv_total, uint64_t seed, int hk, Divisor nv,
@@ -711,27 +719,32 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
         const OffT* soff = reinterpret_cast<const OffT*>(b_off + s_o0);
         mbar_wait(&s_bar, phase);
         phase ^= 1;
-        const uint64_t nchunks = (qn + kPartProbeBlock - 1) / kPartProbeBlock;
         const VT* __restrict__ vp =
             s_kst ? reinterpret_cast<const VT*>(b_val + s_o3) : tvals + tb;  // partition's values
-        auto run = [&](const K* __restrict__ kp, const PEnt* __restrict__ ep) {
+        // J = PJ: probe index type (u32 unless the probe set has >= 2^31 probes)
+        auto run = [&](const K* __restrict__ kp, const PEnt* __restrict__ ep, auto jt) {
+            using J = decltype(jt);
+            using I = OffT;
+            const I tbi = I(tb);
+            const J qj = J(qn);
             // A: counts; (chunk, warp) totals of the first round
             uint64_t mine = 0;
-            const uint64_t i0 = warp * 32 + lane;
-            PEnt nxt = i0 < qn ? ep[i0] : PEnt{};
-            for (uint64_t ch = 0; ch < nchunks; ++ch) {
+            const J nchunks = (qj + J(kPartProbeBlock) - 1) / J(kPartProbeBlock);
+            const J i0 = J(warp * 32 + lane);
+            PEnt nxt = i0 < qj ? ep[i0] : PEnt{};
+            for (J ch = 0; ch < nchunks; ++ch) {
                 K key;
-                uint64_t b, e;
-                const uint64_t i = ch * kPartProbeBlock + i0;
+                I b, e;
+                const J i = ch * J(kPartProbeBlock) + i0;
                 const PEnt cur = nxt;  // entries are prefetched one chunk ahead
-                if (i + kPartProbeBlock < qn) nxt = ep[i + kPartProbeBlock];
+                if (i + J(kPartProbeBlock) < qj) nxt = ep[i + J(kPartProbeBlock)];
                 uint32_t pos;
-                const uint32_t c = pair_count<K, OffT, PEnt, PE, POW2>(kp, cur, soff, i, qn, tb, vb, seed,
-                                                                        hk, nv, compared, key, b, e, pos);
+                const uint32_t c = pair_count<K, OffT, PEnt, PE, POW2, J>(kp, cur, soff, i, qj, tbi, vb, seed,
+                                                                           hk, nv, compared, key, b, e, pos);
                 const uint32_t cw = warp_sum(c);
-                if (ch < kPairRound) {
-                    if (lane == 0) s_wt[ch * nwarps + warp] = cw;
-                    s_info[ch * kPartProbeBlock + i0] = pair_info(b, e, c, pos);
+                if (ch < J(kPairRound)) {
+                    if (lane == 0) s_wt[uint32_t(ch) * nwarps + warp] = cw;
+                    s_info[uint32_t(ch) * kPartProbeBlock + uint32_t(i0)] = pair_info(b, e, c, pos);
                 }
                 mine += cw;
             }
@@ -770,21 +783,22 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
             __syncthreads();
             uint64_t base = s_base;
             // B: rounds of kPairRound chunks
-            for (uint64_t r0 = 0; r0 < nchunks && base < cap; r0 += kPairRound) {
-                const uint64_t r1 = r0 + kPairRound < nchunks ? r0 + kPairRound : nchunks;
+            for (J r0 = 0; r0 < nchunks && base < cap; r0 += J(kPairRound)) {
+                const J r1 = r0 + J(kPairRound) < nchunks ? r0 + J(kPairRound) : nchunks;
                 if (r0 > 0) {
                     __syncthreads();
-                    for (uint64_t ch = r0; ch < r1; ++ch) {
+                    for (J ch = r0; ch < r1; ++ch) {
                         K key;
-                        uint64_t b, e, dummy = 0;
-                        const uint64_t i = ch * kPartProbeBlock + warp * 32 + lane;
-                        const PEnt cur = i < qn ? ep[i] : PEnt{};
+                        I b, e;
+                        uint64_t dummy = 0;
+                        const J i = ch * J(kPartProbeBlock) + i0;
+                        const PEnt cur = i < qj ? ep[i] : PEnt{};
                         uint32_t pos;
-                        const uint32_t c = pair_count<K, OffT, PEnt, PE, POW2>(
-                            kp, cur, soff, i, qn, tb, vb, seed, hk, nv, dummy, key, b, e, pos);
+                        const uint32_t c = pair_count<K, OffT, PEnt, PE, POW2, J>(
+                            kp, cur, soff, i, qj, tbi, vb, seed, hk, nv, dummy, key, b, e, pos);
                         const uint32_t cw = warp_sum(c);
-                        if (lane == 0) s_wt[(ch - r0) * nwarps + warp] = cw;
-                        s_info[(ch - r0) * kPartProbeBlock + warp * 32 + lane] = pair_info(b, e, c, pos);
+                        if (lane == 0) s_wt[uint32_t(ch - r0) * nwarps + warp] = cw;
+                        s_info[uint32_t(ch - r0) * kPartProbeBlock + uint32_t(i0)] = pair_info(b, e, c, pos);
                     }
                 }
                 __syncthreads();
@@ -806,53 +820,54 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
                 }
                 __syncthreads();
                 const uint64_t round_total = s_red[0];
-                const uint64_t ib = r0 * kPartProbeBlock + warp * 32 + lane;
-                PEnt nxtb = ib < qn ? ep[ib] : PEnt{};
-                for (uint64_t ch = r0; ch < r1; ++ch) {
-                    K key;
-                    uint64_t b, e, dummy = 0;
-                    const uint64_t i = ch * kPartProbeBlock + warp * 32 + lane;
+                const J ib = r0 * J(kPartProbeBlock) + i0;
+                PEnt nxtb = ib < qj ? ep[ib] : PEnt{};
+                const uint64_t* wt = s_wt + warp;
+                const uint32_t* inf = s_info + uint32_t(i0);
+                for (J ch = r0; ch < r1; ++ch, wt += nwarps, inf += kPartProbeBlock) {
+                    K key = 0;
+                    I b = 0, e = 0;
+                    uint64_t dummy = 0;
+                    const J i = ch * J(kPartProbeBlock) + i0;
                     const PEnt cur = nxtb;
-                    if (ch + 1 < r1 && i + kPartProbeBlock < qn) nxtb = ep[i + kPartProbeBlock];
-                    const uint32_t info = i < qn ? s_info[(ch - r0) * kPartProbeBlock + warp * 32 + lane] : 0u;
+                    if (ch + 1 < r1 && i + J(kPartProbeBlock) < qj) nxtb = ep[i + J(kPartProbeBlock)];
+                    const uint32_t info = i < qj ? *inf : 0u;
                     const bool walk = info == kNeedWalk;
                     uint32_t c = info & 1u;
-                    b = e = 0;
-                    key = 0;
                     if (__any_sync(0xffffffffu, walk)) {
                         // duplicates / long segments: count again (warp-collective)
                         uint32_t pos;
-                        const uint32_t cc = pair_count<K, OffT, PEnt, PE, POW2>(
-                            kp, cur, soff, i, qn, tb, vb, seed, hk, nv, dummy, key, b, e, pos);
+                        const uint32_t cc = pair_count<K, OffT, PEnt, PE, POW2, J>(
+                            kp, cur, soff, i, qj, tbi, vb, seed, hk, nv, dummy, key, b, e, pos);
                         if (walk) c = cc;
                     }
                     if (!walk) b = e = 0;
-                    const uint32_t incl = warp_inclusive_sum(c);
-                    uint64_t sl = base + s_wt[(ch - r0) * nwarps + warp] + (incl - c);
-                    const uint64_t len = e - b;
-                    const uint64_t pidx = PE::kHasVal && i < qn ? uint64_t(PE::val(cur)) : 0;
+                    const uint32_t incl = warp_incl_count(c);
+                    uint64_t sl = base + *wt + (incl - c);
+                    const I len = e - b;
+                    const uint64_t pidx = PE::kHasVal && i < qj ? uint64_t(PE::val(cur)) : 0;
                     if (!walk && c == 1) {
                         // one match at a known tile key: one value gather + store
                         if (sl < cap) store_pair<PT>(pairs, sl, uint64_t(vp[info >> 16]), pidx);
-                    } else if (c && len <= kLongSeg) {
-                        for (uint64_t t = b; t < e && sl < cap; ++t) {
+                    } else if (c && len <= I(kLongSeg)) {
+                        for (I t = b; t < e && sl < cap; ++t) {
                             if (kp[t] == key) {
                                 store_pair<PT>(pairs, sl, uint64_t(vp[t]), pidx);
                                 ++sl;
                             }
                         }
                     }
-                    uint32_t lm = __ballot_sync(0xffffffffu, c && len > kLongSeg);
+                    uint32_t lm = __ballot_sync(0xffffffffu, c && len > I(kLongSeg));
                     while (lm) {
                         const int src = __ffs(lm) - 1;
                         lm &= lm - 1;
-                        const uint64_t kb = __shfl_sync(0xffffffffu, b, src);
-                        const uint64_t ke = __shfl_sync(0xffffffffu, e, src);
+                        const I kb = __shfl_sync(0xffffffffu, b, src);
+                        const I ke = __shfl_sync(0xffffffffu, e, src);
                         const K kk = __shfl_sync(0xffffffffu, key, src);
                         uint64_t ws = __shfl_sync(0xffffffffu, sl, src);
                         const uint64_t pj = __shfl_sync(0xffffffffu, pidx, src);
-                        for (uint64_t t0 = kb; t0 < ke && ws < cap; t0 += 32) {
-                            const uint64_t t = t0 + lane;
+                        for (I t0 = kb; t0 < ke && ws < cap; t0 += 32) {
+                            const I t = t0 + I(lane);
                             const bool hit = t < ke && kp[t] == kk;
                             const uint32_t hm = __ballot_sync(0xffffffffu, hit);
                             const uint64_t my = ws + __popc(hm & lanemask_lt());
@@ -864,10 +879,13 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
                 base += round_total;
             }
         };
+        auto run_j = [&](const K* __restrict__ kp, const PEnt* __restrict__ ep) {
+            run(kp, ep, PJ(0));
+        };
         if (s_kst && s_pst) {
-            run(reinterpret_cast<const K*>(b_key + s_o1), reinterpret_cast<const PEnt*>(b_ent + s_o2));
+            run_j(reinterpret_cast<const K*>(b_key + s_o1), reinterpret_cast<const PEnt*>(b_ent + s_o2));
         } else {
-            run(s_kst ? reinterpret_cast<const K*>(b_key + s_o1) : tkeys + tb,
+            run_j(s_kst ? reinterpret_cast<const K*>(b_key + s_o1) : tkeys + tb,
                 s_pst ? reinterpret_cast<const PEnt*>(b_ent + s_o2) : pin + q0);
         }
         __syncthreads();
@@ -1096,12 +1114,15 @@ static cudaError_t probe_partitioned(const TableDesc& t, const ProbeArgs& a, cud
             // single pass: counts, look-back over partitions, pairs
             uint64_t* status = pair_off;  // nparts status words
             if ((e = cudaMemsetAsync(status, 0, g.nparts * sizeof(uint64_t), s)) != cudaSuccess) break;
+            // probe indices inside a partition in 32 bits unless the whole
+            // probe set could put 2^31 probes into one partition
+            const bool wide = a.m >= (uint64_t(1) << 31);
             if (a.pair_bytes == 4) {
-                auto kern = k_probe_pairs<K, VT, OffT, IT, POW2, uint32_t>;
-                e = launch_pairs(kern, status);
+                e = wide ? launch_pairs(k_probe_pairs<K, VT, OffT, IT, POW2, uint32_t, uint64_t>, status)
+                         : launch_pairs(k_probe_pairs<K, VT, OffT, IT, POW2, uint32_t, uint32_t>, status);
             } else {
-                auto kern = k_probe_pairs<K, VT, OffT, IT, POW2, uint64_t>;
-                e = launch_pairs(kern, status);
+                e = wide ? launch_pairs(k_probe_pairs<K, VT, OffT, IT, POW2, uint64_t, uint64_t>, status)
+                         : launch_pairs(k_probe_pairs<K, VT, OffT, IT, POW2, uint64_t, uint32_t>, status);
             }
             break;
         }
