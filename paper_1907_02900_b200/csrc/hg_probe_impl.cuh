@@ -361,15 +361,53 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
     }
     uint32_t phase = 0;
     uint64_t matches = 0, compared = 0;
+    // (thread 0) partitions are claimed two ahead and their bounds loaded one
+    // ahead, so the ticket atomic and the dependent bound loads overlap the
+    // previous partition's probes instead of sitting in front of the block
+    // barrier (k8p's top stall)
+    uint32_t p_cur = 0, p_nxt = 0;
+    OffT m_tb = 0, m_te = 0, m_q0 = 0, m_q1 = 0;
+    auto bounds = [&](uint32_t q) {
+        if (q < nparts) {
+            const uint64_t vb = uint64_t(q) << pshift;
+            const uint32_t pv = uint32_t(nv_total - vb < P ? nv_total - vb : uint64_t(P));
+            m_tb = offs[vb];
+            m_te = offs[vb + pv];
+            m_q0 = ppart[q];
+            m_q1 = ppart[q + 1];
+        }
+    };
+    // (count-only; the per-probe-count / pair modes keep their registers)
+    constexpr bool kAhead = MODE == 0;
+    if (kAhead && tid == 0) {
+        p_cur = atomicAdd(ticket, 1u);
+        p_nxt = atomicAdd(ticket, 1u);
+        bounds(p_cur);
+    }
     while (true) {
         if (tid == 0) {
-            const uint64_t p = atomicAdd(ticket, 1u);
+            uint64_t p, tb = 0, te = 0, q0 = 0, q1 = 0;
+            if constexpr (kAhead) {
+                p = p_cur;
+                tb = m_tb, te = m_te, q0 = m_q0, q1 = m_q1;
+                p_cur = p_nxt;
+                bounds(p_cur);
+                if (p_nxt < nparts) p_nxt = atomicAdd(ticket, 1u);
+            } else {
+                p = atomicAdd(ticket, 1u);
+                if (p < nparts) {
+                    const uint64_t vb = p << pshift;
+                    const uint32_t pv = uint32_t(nv_total - vb < P ? nv_total - vb : uint64_t(P));
+                    tb = offs[vb];
+                    te = offs[vb + pv];
+                    q0 = ppart[p];
+                    q1 = ppart[p + 1];
+                }
+            }
             s_p = p;
             if (p < nparts) {
                 const uint64_t vb = p << pshift;
                 const uint32_t pv = uint32_t(nv_total - vb < P ? nv_total - vb : uint64_t(P));
-                const uint64_t tb = offs[vb], te = offs[vb + pv];
-                const uint64_t q0 = ppart[p], q1 = ppart[p + 1];
                 const uint64_t qin = slack_in ? p * in_cap : q0;
                 s_tb = tb; s_te = te; s_q0 = q0; s_q1 = q1; s_qin = qin;
                 s_kst = te - tb <= kcap;
