@@ -505,7 +505,7 @@ def run_b200(args):
     torch.cuda.synchronize()
     nv = hg.derived_vertex_count(n, 1.0)
     if world > 1:
-        engine.exchange_events = []  # time the all-to-alls of the timed steps
+        engine.exchange_events = None  # the timed steps run un-instrumented
 
     def barrier():
         if world > 1:
@@ -513,8 +513,12 @@ def run_b200(args):
         torch.cuda.synchronize()
 
     # ---- timed region (device-resident inputs; each input 1 GiB > 126 MB L2)
+    # The step time comes from this un-instrumented region; the per-kernel
+    # averages (roofline, launch count) from an identical pass right after it
+    # with the library's event timeline on (its 2 events per launch cost ~2 %
+    # of the step, so they stay out of `value`).
     dbg = os.environ.get("BENCH_DEBUG", "")
-    _lib.profiler_enable("noprof" not in dbg)
+    _lib.profiler_enable(False)
     _lib.profiler_collect()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local if "noclock" not in dbg else 10 ** 6)
@@ -530,9 +534,16 @@ def run_b200(args):
                 log(f"step host {1e3 * (time.perf_counter() - h0):.1f} ms")
         ev1.record(stream)
         barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    _lib.profiler_enable("noprof" not in dbg)
+    _lib.profiler_collect()
+    if world > 1:
+        engine.exchange_events = []  # the exchange timing comes from the instrumented pass too
+    for _ in range(args.steps):
+        step()
+    barrier()
     _lib.profiler_enable(False)
     kern = _lib.profiler_collect()
-    ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -565,6 +576,9 @@ def run_b200(args):
     local_n = n if world == 1 else int(engine.last_local_n)
     local_m = m if world == 1 else int(engine.last_local_m)
     local_v = nv if world == 1 else int(engine.local_vertices)
+    if not kern:  # BENCH_DEBUG=noprof: step time only
+        print(json.dumps({"ms_per_step": round(ms, 4), "value": round(value, 3)}))
+        return
     dom = max((k for k in kern if alg_bytes(k, 1, 1, 1, 1) > 0), key=lambda k: kern[k][1])
     dl, dms = kern[dom]
     avg_ms = dms / dl
@@ -582,6 +596,7 @@ def run_b200(args):
                 "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                 "alg_bytes_per_launch": ab, "avg_launch_ms": round(avg_ms, 4),
                 "peak_source": peak_src,
+                "launch_times": "library CUDA-event timeline over K instrumented steps run right after the un-instrumented timed region",
                 "step_alg_bytes": sum(alg_bytes(k, local_n, local_v, local_m, comparisons)
                                       for k in kern)}
     ref_bytes = reference_alg_bytes(args.variant, local_n, local_v, local_m,
