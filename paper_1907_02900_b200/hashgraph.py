@@ -439,7 +439,7 @@ def _join_options(opts: ProbeOptions, cap_bound: int):
     o.pair_cap = int(opts.pair_cap)
     pairs = None
     if opts.materialize:
-        pairs = np.zeros(max(min(int(opts.pair_cap), cap_bound), 0), MATCH_PAIR_DTYPE)
+        pairs = np.empty(max(min(int(opts.pair_cap), cap_bound), 0), MATCH_PAIR_DTYPE)
         o.pairs = pairs.ctypes.data if pairs.size else None
         if pairs.size == 0:
             o.pair_cap = 0
