@@ -1,5 +1,4 @@
-set -x
-nvidia-smi -L; nproc
-timeout 900 python bench.py --steps 10 --warmup 3 --csv=gpurun_out/r02d_bench_rows.csv > gpurun_out/r02d_bench_full.json 2> gpurun_out/r02d_bench_full.err; tail -2 gpurun_out/r02d_bench_full.err
-timeout 600 python bench.py --config c5 --steps 3 --warmup 3 --no-cpu --no-extras --csv= > gpurun_out/r02d_bench_c5.json 2> gpurun_out/r02d_bench_c5.err; tail -2 gpurun_out/r02d_bench_c5.err
-bash scripts/gpu_prof.sh r02d
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/gputest.log 2>&1; tail -3 gpurun_out/gputest.log
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-extras --csv= 2>/dev/null | tail -1 > gpurun_out/ab.json
+python -c "import json; d=json.load(open('gpurun_out/ab.json')); print(d['ms_per_step'], d['value'], d['gpu_launches'], d['e2e']['value'], d['roofline']['frac'], d['roofline']['step_reference_frac'])"
