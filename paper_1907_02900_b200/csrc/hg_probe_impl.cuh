@@ -701,6 +701,7 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
     __shared__ uint32_t s_o0, s_o1, s_o2, s_o3, s_kst, s_pst;
     __shared__ uint64_t s_wt[kPairRound * nwarps];
     __shared__ uint64_t s_red[nwarps];
+    __shared__ uint64_t s_rt;  // a round's pair total
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
         mbar_init(&s_bar, 1);
@@ -763,6 +764,23 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
         auto run = [&](const K* __restrict__ kp, const PEnt* __restrict__ ep, auto jt) {
             using J = decltype(jt);
             using I = OffT;
+            // (one warp) exclusive scan of a round's (chunk, warp) totals in
+            // (chunk, warp) order, relative to the round's base; s_rt = total
+            auto scan_round = [&]() {
+                constexpr uint32_t per = kPairRound * nwarps / 32;
+                uint64_t x[per];
+                uint64_t sum = 0;
+#pragma unroll
+                for (uint32_t k = 0; k < per; ++k) sum += (x[k] = s_wt[lane * per + k]);
+                const uint64_t inc = warp_inclusive_sum(sum);
+                uint64_t run_ = inc - sum;
+#pragma unroll
+                for (uint32_t k = 0; k < per; ++k) {
+                    s_wt[lane * per + k] = run_;
+                    run_ += x[k];
+                }
+                if (lane == 31) s_rt = inc;
+            };
             const I tbi = I(tb);
             const J qj = J(qn);
             // A: counts; (chunk, warp) totals of the first round
@@ -817,6 +835,8 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
                     s_base = prefix;
                     matches += tot;
                 }
+            } else if (warp == 1) {
+                scan_round();  // round 0, overlapping warp 0's look-back
             }
             __syncthreads();
             uint64_t base = s_base;
@@ -838,26 +858,11 @@ k_probe_pairs(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __r
                         if (lane == 0) s_wt[uint32_t(ch - r0) * nwarps + warp] = cw;
                         s_info[uint32_t(ch - r0) * kPartProbeBlock + uint32_t(i0)] = pair_info(b, e, c, pos);
                     }
+                    __syncthreads();
+                    if (warp == 0) scan_round();
+                    __syncthreads();
                 }
-                __syncthreads();
-                if (warp == 0) {
-                    // exclusive scan of (r1 - r0) * nwarps totals in (chunk, warp) order
-                    constexpr uint32_t per = kPairRound * nwarps / 32;
-                    uint64_t x[per];
-                    uint64_t sum = 0;
-#pragma unroll
-                    for (uint32_t k = 0; k < per; ++k) sum += (x[k] = s_wt[lane * per + k]);
-                    const uint64_t inc = warp_inclusive_sum(sum);
-                    uint64_t run_ = inc - sum;
-#pragma unroll
-                    for (uint32_t k = 0; k < per; ++k) {
-                        s_wt[lane * per + k] = run_;  // relative to the round's base
-                        run_ += x[k];
-                    }
-                    if (lane == 31) s_red[0] = inc;  // round total
-                }
-                __syncthreads();
-                const uint64_t round_total = s_red[0];
+                const uint64_t round_total = s_rt;
                 const J ib = r0 * J(kPartProbeBlock) + i0;
                 PEnt nxtb = ib < qj ? ep[ib] : PEnt{};
                 const uint64_t* wt = s_wt + warp;
