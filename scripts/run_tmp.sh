@@ -1,2 +1,2 @@
-timeout 900 python bench.py --steps 10 --warmup 3 --csv=gpurun_out/r02d_bench_rows.csv > gpurun_out/r02d_bench_full.json 2> gpurun_out/r02d_bench_full.err; tail -1 gpurun_out/r02d_bench_full.err
-python -c "import json; d=json.load(open('gpurun_out/r02d_bench_full.json')); print(d['ms_per_step'], d['value'], d['e2e']['value'], d['roofline']['frac'], d['roofline']['step_reference_frac'], {k: v.get('gprobes_s') for k, v in d['phases']['c4_join'].items() if isinstance(v, dict)})"
+timeout 300 python scripts/prof_c3.py 28 > gpurun_out/c3prof.txt 2>&1; head -1 gpurun_out/c3prof.txt
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/gputest.log 2>&1; tail -3 gpurun_out/gputest.log
