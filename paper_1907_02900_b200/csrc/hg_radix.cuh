@@ -206,6 +206,15 @@ constexpr int kSplitBlock = 512;
 #define HG_SPLIT_STAGES 2
 #endif
 constexpr int kSplitStages = HG_SPLIT_STAGES;  // TMA input stages (one tile prefetched ahead)
+#ifndef HG_P2_STAGES
+#define HG_P2_STAGES kSplitStages
+#endif
+#ifndef HG_P2_ITEMS_Q
+#define HG_P2_ITEMS_Q 4  // pass-2 items per thread = the pass-1 count * Q / 4
+#endif
+// TMA input stages of a pass
+template <bool PASS2>
+__host__ __device__ constexpr int split_stages() { return PASS2 ? HG_P2_STAGES : kSplitStages; }
 constexpr int kMaxDigits = 256;
 constexpr uint32_t kOwnerRun = 64;  // digit runs up to this long are filled by their owner
 // Consumer threads of a pass: pass 2 runs one producer warp (TMA refills)
@@ -215,8 +224,10 @@ __host__ __device__ constexpr int split_cons() { return PASS2 ? kSplitBlock - 32
 // 16 / 8 / 4 entries per consumer thread for 4- / 8- / 16-byte entries.
 template <typename E>
 __host__ __device__ constexpr int split_items() { return sizeof(E) >= 16 ? 4 : sizeof(E) <= 4 ? 16 : 8; }
+template <typename E, bool PASS2>
+__host__ __device__ constexpr int pass_items() { return PASS2 ? split_items<E>() * HG_P2_ITEMS_Q / 4 : split_items<E>(); }
 template <typename E, bool PASS2 = false>
-__host__ __device__ constexpr int split_tile() { return split_cons<PASS2>() * split_items<E>(); }
+__host__ __device__ constexpr int split_tile() { return split_cons<PASS2>() * pass_items<E, PASS2>(); }
 
 // One radix pass. RAW: input is the raw key array (+ optional vals, else the
 // input position is the value). Otherwise input is an entry array.
@@ -233,10 +244,11 @@ template <typename K, typename VT, bool RAW, bool PASS2 = false>
 struct SplitLayout {
     using E = typename EntryT<K, VT>::T;
     using InT = typename std::conditional<RAW, K, E>::type;
-    static constexpr int kItems = split_items<E>();
+    static constexpr int kItems = pass_items<E, PASS2>();
     static constexpr int kTile = split_tile<E, PASS2>();
+    static constexpr int kStages = split_stages<PASS2>();
     static constexpr size_t kInBytes = (size_t(kTile) * sizeof(InT) + 32 + 15) & ~size_t(15);
-    static constexpr size_t kBytes = kSplitStages * kInBytes + size_t(kTile) * sizeof(E) + kTile + 16;
+    static constexpr size_t kBytes = kStages * kInBytes + size_t(kTile) * sizeof(E) + kTile + 16;
 };
 
 // CTAs per SM the layout allows (<= 227 KB of shared memory per SM): 3 when
@@ -268,6 +280,7 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
     using ET = EntryT<K, VT>;
     using E = typename ET::T;
     using L = SplitLayout<K, VT, RAW, PASS2>;
+    constexpr int kSt = L::kStages;
     using InT = typename L::InT;
     constexpr int kItems = L::kItems;
     constexpr int kTile = L::kTile;
@@ -280,12 +293,12 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
     constexpr bool kProd = PASS2;
     constexpr uint32_t kCons = split_cons<PASS2>();
     extern __shared__ __align__(128) unsigned char smem[];
-    E* const s_ent = reinterpret_cast<E*>(smem + kSplitStages * L::kInBytes);
+    E* const s_ent = reinterpret_cast<E*>(smem + kSt * L::kInBytes);
     uint8_t* const s_dig = reinterpret_cast<uint8_t*>(s_ent + kTile);
-    __shared__ uint64_t s_bar[kSplitStages];    // stage full (TMA landed)
-    __shared__ uint64_t s_empty[kSplitStages];  // stage consumed (producer mode)
-    __shared__ uint64_t s_t0[kSplitStages], s_t1[kSplitStages], s_cb[kSplitStages];
-    __shared__ uint32_t s_ofs[kSplitStages], s_ok[kSplitStages];
+    __shared__ uint64_t s_bar[kSt];    // stage full (TMA landed)
+    __shared__ uint64_t s_empty[kSt];  // stage consumed (producer mode)
+    __shared__ uint64_t s_t0[kSt], s_t1[kSt], s_cb[kSt];
+    __shared__ uint32_t s_ofs[kSt], s_ok[kSt];
     __shared__ uint32_t s_cnt[kMaxDigits];
     __shared__ uint32_t s_long[kMaxDigits];  // digits whose run is filled cooperatively
     __shared__ uint32_t s_nlong;
@@ -362,13 +375,13 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
     };
 
     if (tid == 0) {
-        for (int st = 0; st < kSplitStages; ++st) {
+        for (int st = 0; st < kSt; ++st) {
             mbar_init(&s_bar[st], 1);
             mbar_init(&s_empty[st], 1);
         }
         fence_mbar_init();
         if constexpr (!kProd)
-            for (int st = 0; st < kSplitStages - 1; ++st) issue(blockIdx.x + uint64_t(st) * gridDim.x, st, 0u);
+            for (int st = 0; st < kSt - 1; ++st) issue(blockIdx.x + uint64_t(st) * gridDim.x, st, 0u);
     }
     __syncthreads();
     if constexpr (kProd) {
@@ -376,9 +389,9 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
             if (tid == kCons) {
                 uint32_t abort = 0;
                 for (uint64_t i = 0;; ++i) {
-                    const int sp = int(i % kSplitStages);
-                    if (i >= uint64_t(kSplitStages))
-                        mbar_wait(&s_empty[sp], uint32_t((i / kSplitStages - 1) & 1));
+                    const int sp = int(i % kSt);
+                    if (i >= uint64_t(kSt))
+                        mbar_wait(&s_empty[sp], uint32_t((i / kSt - 1) & 1));
                     issue(blockIdx.x + i * gridDim.x, sp, abort);
                     if (!s_ok[sp]) {
                         mbar_arrive(&s_bar[sp]);  // releases s_ok = 0: the consumers stop
@@ -417,9 +430,9 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
         } else {
             if (!s_ok[st]) break;
             // refill the stage consumed in the previous iteration
-            const int pf = st == 0 ? kSplitStages - 1 : st - 1;
+            const int pf = st == 0 ? kSt - 1 : st - 1;
             if (tid == 0) {
-                issue(tile + uint64_t(kSplitStages - 1) * gridDim.x, pf, ovf);
+                issue(tile + uint64_t(kSt - 1) * gridDim.x, pf, ovf);
                 if (kPoll && out_cap && (++iter & 15) == 0) ovf = *reinterpret_cast<volatile const uint32_t*>(overflow);
             }
             mbar_wait(&s_bar[st], phase);
@@ -555,7 +568,7 @@ k_multisplit(const void* __restrict__ in, const VT* __restrict__ vals, uint64_t 
         if constexpr (kProd) {
             if (tid == 0) mbar_arrive(&s_empty[st]);  // stage st free for the producer
         }
-        if (++st == kSplitStages) {
+        if (++st == kSt) {
             st = 0;
             phase ^= 1;
         }

@@ -1,2 +1,3 @@
-timeout 300 python scripts/prof_c3.py 28 > gpurun_out/c3prof.txt 2>&1; head -1 gpurun_out/c3prof.txt
-timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/gputest.log 2>&1; tail -3 gpurun_out/gputest.log
+bash scripts/ab.sh exp/libp2s3.so
+HG_B200_LIB=exp/libp2s3.so timeout 300 python scripts/prof_c3.py 28 2>&1 | grep -v "C3 v1"
+timeout 300 python scripts/prof_c3.py 28 2>&1 | grep -v "C3 v1"
