@@ -251,7 +251,7 @@ struct HeavyItem {
     uint64_t begin;  // first table entry (global index) of the chunk
     uint64_t pidx;   // probe position (per-probe counts)
     uint32_t len;    // comparisons in the chunk (0: unused slot)
-    uint32_t pad;
+    uint32_t mult;   // probes sharing this (segment, key) walk (count-only; 0 = 1)
 };
 
 struct HeavyQueue {
@@ -267,7 +267,7 @@ struct HeavyQueue {
 // always written.
 template <typename K>
 __device__ __forceinline__ bool defer_heavy(const HeavyQueue& q, K key, uint64_t gb, uint64_t len,
-                                            uint64_t pidx) {
+                                            uint64_t pidx, uint32_t mult = 1) {
     if (q.items == nullptr || len <= kHeavySeg) return false;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t nch = uint32_t((len + kHeavyChunk - 1) / kHeavyChunk);
@@ -283,7 +283,7 @@ __device__ __forceinline__ bool defer_heavy(const HeavyQueue& q, K key, uint64_t
         it.len = ok ? uint32_t(len - uint64_t(c) * kHeavyChunk < kHeavyChunk
                                    ? len - uint64_t(c) * kHeavyChunk : kHeavyChunk)
                     : 0u;
-        it.pad = 0;
+        it.mult = mult;
         q.items[slot + c] = it;
     }
     return ok;
@@ -315,7 +315,8 @@ k_heavy_walk(const HeavyItem* __restrict__ items, const uint32_t* __restrict__ n
             x = warp_sum(x);
             if (lane == 0 && x) {
                 if constexpr (COUNTS) atomicAdd(counts + it.pidx, x);
-                atomicAdd(reinterpret_cast<unsigned long long*>(totals), (unsigned long long)x);
+                const unsigned long long mx = (unsigned long long)x * (it.mult ? it.mult : 1u);
+                atomicAdd(reinterpret_cast<unsigned long long*>(totals), mx);
             }
         }
         __syncthreads();
@@ -355,10 +356,21 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
     __shared__ uint32_t s_o0, s_o1, s_o2, s_kst, s_pst;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr uint32_t nwarps = kPartProbeBlock / 32;
+    // count-only: the partition's heavy (segment, key) walks, deduplicated --
+    // every probe of a key gets the same count, so each distinct key's heavy
+    // segment is queued once with its probe multiplicity (C3: the 16 probes
+    // of a Zipf rank no longer re-read its segment 16 times). Full table:
+    // queued per probe as before.
+    constexpr uint32_t kDedup = MODE == 0 ? 64 : 1;
+    __shared__ uint64_t s_dk[kDedup];
+    __shared__ uint32_t s_db[kDedup], s_dl[kDedup], s_dm[kDedup], s_dv[kDedup];
+    __shared__ uint32_t s_dn;
     if (tid == 0) {
         mbar_init(&s_bar, 1);
         fence_mbar_init();
+        s_dn = 0;
     }
+    if (tid < kDedup) s_dv[tid] = 0;
     uint32_t phase = 0;
     uint64_t matches = 0, compared = 0;
     // (thread 0) partitions are claimed two ahead and their bounds loaded one
@@ -474,6 +486,33 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
                         const I kb = __shfl_sync(0xffffffffu, b, src);
                         const I ke = __shfl_sync(0xffffffffu, e, src);
                         const K kk = __shfl_sync(0xffffffffu, key, src);
+                        if (heavy.items && uint64_t(ke - kb) > kHeavySeg && uint64_t(ke) < (uint64_t(1) << 32)) {
+                            // known key: one more probe on its walk
+                            const uint32_t dn = min(*reinterpret_cast<volatile uint32_t*>(&s_dn), kDedup);
+                            uint32_t hit = 0;
+                            for (uint32_t j0 = 0; j0 < dn && !hit; j0 += 32) {
+                                const uint32_t j = j0 + lane;
+                                const bool m = j < dn && reinterpret_cast<volatile uint32_t*>(s_dv)[j] &&
+                                               reinterpret_cast<volatile uint64_t*>(s_dk)[j] == uint64_t(kk);
+                                hit = __ballot_sync(0xffffffffu, m);
+                                if (hit && lane == uint32_t(__ffs(hit) - 1)) atomicAdd(&s_dm[j], 1u);
+                            }
+                            if (hit) continue;
+                            uint32_t slot = 0;
+                            if (lane == 0) slot = atomicAdd(&s_dn, 1u);
+                            slot = __shfl_sync(0xffffffffu, slot, 0);
+                            if (slot < kDedup) {
+                                if (lane == 0) {
+                                    s_dk[slot] = uint64_t(kk);
+                                    s_db[slot] = uint32_t(kb);
+                                    s_dl[slot] = uint32_t(ke - kb);
+                                    s_dm[slot] = 1;
+                                    __threadfence_block();
+                                    reinterpret_cast<volatile uint32_t*>(s_dv)[slot] = 1;
+                                }
+                                continue;
+                            }
+                        }
                         if (defer_heavy(heavy, kk, tb + uint64_t(kb), uint64_t(ke - kb), 0)) continue;
                         uint32_t cc = 0;
                         for (I t = kb + I(lane); t < ke; t += 32) cc += kp[t] == kk;
@@ -485,6 +524,25 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
                 I base = I(warp) * 32;
                 for (; base + 32 <= qi; base += I(nwarps) * 32) round(base, std::false_type{});
                 if (base < qi) round(base, std::true_type{});
+                if (heavy.items) {
+                    // queue the partition's deduplicated heavy walks (warp 0)
+                    __syncthreads();
+                    if (warp == 0) {
+                        const uint32_t dn = min(s_dn, kDedup);
+                        for (uint32_t j = 0; j < dn; ++j) {
+                            const K kk = K(s_dk[j]);
+                            const I kb = I(s_db[j]), ke = kb + I(s_dl[j]);
+                            const uint32_t mult = s_dm[j];
+                            if (defer_heavy(heavy, kk, tb + uint64_t(kb), uint64_t(ke - kb), 0, mult)) continue;
+                            uint32_t cc = 0;  // queue full: walk here
+                            for (I t = kb + I(lane); t < ke; t += 32) cc += kp[t] == kk;
+                            cc = warp_sum(cc);
+                            if (lane == 0) matches += uint64_t(cc) * mult;
+                        }
+                        if (lane == 0) s_dn = 0;
+                        for (uint32_t j = lane; j < kDedup; j += 32) s_dv[j] = 0;
+                    }
+                }
             } else {
                 for (uint64_t base = uint64_t(warp) * 32; base < qn; base += uint64_t(nwarps) * 32) {
                     const uint64_t i = base + lane;

@@ -1,3 +1,9 @@
-bash scripts/ab.sh exp/libp2s3.so
-HG_B200_LIB=exp/libp2s3.so timeout 300 python scripts/prof_c3.py 28 2>&1 | grep -v "C3 v1"
-timeout 300 python scripts/prof_c3.py 28 2>&1 | grep -v "C3 v1"
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/gputest.log 2>&1; tail -3 gpurun_out/gputest.log
+timeout 900 python bench.py --steps 10 --warmup 3 --csv=gpurun_out/r02e_bench_rows.csv > gpurun_out/r02e_bench_full.json 2> gpurun_out/r02e_bench_full.err; tail -1 gpurun_out/r02e_bench_full.err
+python - <<'PY'
+import json
+d=json.load(open('gpurun_out/r02e_bench_full.json'))
+print(d['ms_per_step'], d['value'], d['e2e']['value'], d['roofline']['frac'], d['roofline']['step_reference_frac'])
+for L,x in d['phases']['c3_zipf'].items():
+    if isinstance(x, dict): print(L, x['v2']['build_gkeys_s'], x['probe']['probe_ms'], x['probe']['gprobes_s'], x['probe']['match_count'], x['probe']['key_comparisons'])
+PY
