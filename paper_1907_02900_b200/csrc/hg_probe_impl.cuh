@@ -360,8 +360,10 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
     // every probe of a key gets the same count, so each distinct key's heavy
     // segment is queued once with its probe multiplicity (C3: the 16 probes
     // of a Zipf rank no longer re-read its segment 16 times). Full table:
-    // queued per probe as before.
-    constexpr uint32_t kDedup = MODE == 0 ? 64 : 1;
+    // queued per probe as before. Compiled for u64-key tables only: on the
+    // u32 C2 probe the partition-end flush barrier alone cost k8p 2.4 %.
+    constexpr bool kDedupOn = MODE == 0 && sizeof(K) == 8;
+    constexpr uint32_t kDedup = kDedupOn ? 64 : 1;
     __shared__ uint64_t s_dk[kDedup];
     __shared__ uint32_t s_db[kDedup], s_dl[kDedup], s_dm[kDedup], s_dv[kDedup];
     __shared__ uint32_t s_dn;
@@ -486,7 +488,7 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
                         const I kb = __shfl_sync(0xffffffffu, b, src);
                         const I ke = __shfl_sync(0xffffffffu, e, src);
                         const K kk = __shfl_sync(0xffffffffu, key, src);
-                        if (heavy.items && uint64_t(ke - kb) > kHeavySeg && uint64_t(ke) < (uint64_t(1) << 32)) {
+                        if (kDedupOn && heavy.items && uint64_t(ke - kb) > kHeavySeg && uint64_t(ke) < (uint64_t(1) << 32)) {
                             // known key: one more probe on its walk
                             const uint32_t dn = min(*reinterpret_cast<volatile uint32_t*>(&s_dn), kDedup);
                             uint32_t hit = 0;
@@ -524,7 +526,7 @@ k_probe_part(const typename EntryT<K, IT>::T* __restrict__ pin, const OffT* __re
                 I base = I(warp) * 32;
                 for (; base + 32 <= qi; base += I(nwarps) * 32) round(base, std::false_type{});
                 if (base < qi) round(base, std::true_type{});
-                if (heavy.items) {
+                if (kDedupOn && heavy.items) {
                     // queue the partition's deduplicated heavy walks (warp 0)
                     __syncthreads();
                     if (warp == 0) {
